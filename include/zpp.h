@@ -1,0 +1,169 @@
+/*
+ * zpp.h -- C ABI of the B200-native ZeRO++ communication-reduction hot path
+ * (libzpp.so, sm_100a).
+ *
+ * The reference (zerosim, pure Python/numpy, /root/reference/pkg/src/zerosim)
+ * has no FFI; its plugin point for this path is the codec object plus the
+ * module-level functions re-exported from zerosim/__init__.py.  Each entry
+ * point below replaces the compute of one of those reference functions; the
+ * Python package paper_2306_10209_b200 binds them through ctypes and keeps the
+ * reference's names, argument meaning and exceptions.
+ *
+ * Conventions
+ *   - Plain pointers and sizes only.  Every pointer is a device pointer unless
+ *     stated otherwise; `stream` is a cudaStream_t (NULL = legacy stream).
+ *   - All launches are asynchronous and stream-ordered.  The caller owns every
+ *     buffer (the library allocates nothing on the hot path; only
+ *     zpp_comm_create allocates the symmetric workspace).
+ *   - Host-detectable errors (config, shapes) are returned synchronously.
+ *     Device-detected conditions are OR-ed into *errflag (a device uint32):
+ *       ZPP_FLAG_NONFINITE -> reference ValidationError (zs/quantizer.py:73-74)
+ *       ZPP_FLAG_BADCODE   -> reference IntegrityError  (zs/quantizer.py:234-235)
+ *       ZPP_FLAG_TIMEOUT   -> a peer never reached a device barrier
+ *     errflag may be NULL (conditions are then not reported).
+ *   - Wire format of one quantized tensor of n elements, block B, b bits:
+ *       codes : ceil(n/B)*B*b/8 bytes, INT8 two's complement or INT4 two
+ *               nibbles per byte, low nibble first (zs/quantizer.py:185-189),
+ *               zero padding of the last block included;
+ *       absmax: ceil(n/B) per-block max|x| as fp32 (inputs fp16/bf16/fp32:
+ *               exact) or f64 (f64 inputs and fused requantization outputs).
+ *     The reference scale is f64(absmax)/qmax, bit-exact (zpp_scales).
+ */
+#ifndef ZPP_H_
+#define ZPP_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes <-> zs/errors.py:9-30 */
+enum {
+  ZPP_OK = 0,
+  ZPP_ERR_CONFIG = 1,     /* ConfigError     */
+  ZPP_ERR_VALIDATION = 2, /* ValidationError */
+  ZPP_ERR_INTEGRITY = 3,  /* IntegrityError  */
+  ZPP_ERR_CUDA = 4,
+  ZPP_ERR_COMM = 5
+};
+
+/* element types */
+enum { ZPP_F32 = 0, ZPP_F16 = 1, ZPP_BF16 = 2, ZPP_F64 = 3 };
+
+/* device error flag bits */
+enum { ZPP_FLAG_NONFINITE = 1, ZPP_FLAG_BADCODE = 2, ZPP_FLAG_TIMEOUT = 4 };
+
+int zpp_version(void);
+const char* zpp_last_error(void);
+int zpp_device_sm_count(void);
+
+/* ---- codec ------------------------------------------------------------ */
+
+/* K0  quantize(FlatTensor, QuantConfig)            zs/quantizer.py:204-228
+ * x: n elements of dtype; absmax: fp32 for F32/F16/BF16 inputs, f64 for F64.
+ * block = QuantConfig.block_size, or the effective full_tensor block
+ * (zs/quantizer.py:179-182) computed by the caller. */
+int zpp_quantize(const void* x, int dtype, int64_t n, int bits, int64_t block, void* codes, void* absmax,
+                 void* errflag, void* stream);
+
+/* K1  qgZ hop-1 encode of one stage                zs/collectives.py:509-518
+ * grad: n elements (one rank's full gradient bucket); writes the send buffer
+ * [j < X][c < Y][e < L] (L = n / (S*X*Y)) quantized in blocks of `block`
+ * (L % block == 0).  reorder != 0 applies reorder_mapping's inverse
+ * (zs/collectives.py:407-417, :498-499); reorder == 0 reproduces the
+ * reference's reorder=False routing. */
+int zpp_swizzle_quantize(const void* grad, int dtype, int64_t n, int X, int Y, int S, int stage, int reorder,
+                         int bits, int64_t block, void* codes, void* absmax, void* errflag, void* stream);
+
+/* K4  dequantize(QuantizedTensor)                  zs/quantizer.py:231-238
+ * out: n elements of out_dtype, each the correctly rounded f64 code*scale. */
+int zpp_dequantize(const void* codes, const void* absmax, int absmax_dtype, int64_t n, int bits, int64_t block,
+                   void* out, int out_dtype, void* errflag, void* stream);
+
+/* K4  gather-dequantize: the receive side of all_gather_qwz
+ * (zs/collectives.py:264).  codes[s]/absmax[s] (host arrays of n_src device
+ * pointers, local or NVLink peer) are decoded into out[s*shard_len ...].
+ * rot staggers which source each warp starts with.  Optional hpZ
+ * write-through: out elements [sec_lo, sec_lo+sec_len) are also written to
+ * sec_out (NULL to skip). */
+int zpp_gather_dequantize(const void* const* codes, const void* const* absmax, int absmax_dtype, int n_src,
+                          int rot, int64_t shard_len, int bits, int64_t block, void* out, int out_dtype,
+                          void* sec_out, int64_t sec_lo, int64_t sec_len, void* errflag, void* stream);
+
+/* K3  BlockCodec.reduce_final                      zs/collectives.py:71-75
+ * out[i] = post_scale * fold_{s ascending}(+0.0, code_s[i]*scale_s) in f64. */
+int zpp_dequant_reduce(const void* const* codes, const void* const* absmax, int absmax_dtype, int n_src, int64_t n,
+                       int bits, int64_t block, void* out, int out_dtype, double post_scale, void* errflag,
+                       void* stream);
+
+/* K2  fused_dequant_reduce_quant                   zs/quantizer.py:241-258
+ * n_src inputs of n elements (in_bits/in_block) -> one tensor quantized with
+ * out_bits/out_block; out_absmax is f64.  workspace (device) of
+ * zpp_drq_workspace_bytes(n, out_block) bytes, may be NULL when that is 0. */
+int zpp_dequant_reduce_quant(const void* const* codes, const void* const* absmax, int absmax_dtype, int n_src,
+                             int64_t n, int in_bits, int64_t in_block, int out_bits, int64_t out_block,
+                             void* out_codes, void* out_absmax, void* workspace, size_t workspace_bytes,
+                             void* errflag, void* stream);
+size_t zpp_drq_workspace_bytes(int64_t n, int64_t out_block);
+
+/* QuantizedTensor.scales: f64(absmax)/qmax, bit-exact (zs/quantizer.py:219) */
+int zpp_scales(const void* absmax, int absmax_dtype, int64_t n_blocks, int bits, void* out_f64, void* stream);
+
+/* ---- multi-GPU (one process per GPU, NVLink P2P over CUDA IPC) ---------- */
+
+typedef struct zpp_comm* zpp_comm_t;
+#define ZPP_IPC_HANDLE_BYTES 64
+
+/* Allocates `sym_bytes` of device memory that every rank maps (symmetric
+ * workspace) plus barrier flags.  group_size = GPUs per group (the
+ * reference's gpus_per_node, zs/topology.py:31-52). */
+int zpp_comm_create(int rank, int world, int group_size, size_t sym_bytes, zpp_comm_t* out);
+/* this rank's IPC handle (ZPP_IPC_HANDLE_BYTES bytes, host memory) */
+int zpp_comm_ipc_handle(zpp_comm_t comm, void* handle_out);
+/* all ranks' handles, world * ZPP_IPC_HANDLE_BYTES bytes in rank order (host) */
+int zpp_comm_open_peers(zpp_comm_t comm, const void* all_handles);
+/* device address (in this process) of `rank`'s symmetric buffer */
+void* zpp_comm_sym_ptr(zpp_comm_t comm, int rank);
+size_t zpp_comm_sym_bytes(zpp_comm_t comm);
+/* device barrier among ranks: scope 0 = world, 1 = my group, 2 = my cross set
+ * (same local index in every group).  Bounded spin (timeout_ms). */
+int zpp_comm_barrier(zpp_comm_t comm, int scope, int timeout_ms, void* errflag, void* stream);
+int zpp_comm_destroy(zpp_comm_t comm);
+
+/* qwZ all-gather, fused over NVLink (zs/collectives.py:244-282):
+ * quantize this rank's shard into the symmetric buffer, world barrier, then
+ * every rank decodes all W shards by peer loads straight into out
+ * (W*shard_len elements).  Optional hpZ write-through of
+ * out[sec_lo, sec_lo+sec_len) into sec_out. */
+int zpp_qwz_allgather(zpp_comm_t comm, size_t sym_offset, const void* shard, int dtype, int64_t shard_len, int bits,
+                      int64_t block, void* out, int out_dtype, void* sec_out, int64_t sec_lo, int64_t sec_len,
+                      void* errflag, void* stream);
+
+/* hpZ secondary-partition all-gather inside the group over NVLink
+ * (zs/collectives.py:202-241 with groups = PartitionSpec.groups()):
+ * every rank's secondary shard (sec_len elements of elem_bytes) is held in
+ * HBM at byte sym_offset of its symmetric buffer (written there by the qwZ
+ * write-through, zs/engine.py:364-367); out receives the group's shards in
+ * member order. */
+int zpp_hpz_allgather(zpp_comm_t comm, size_t sym_offset, int64_t sec_len, int elem_bytes, void* out,
+                      void* errflag, void* stream);
+
+/* qgZ 2-hop quantized reduce-scatter over NVLink (zs/collectives.py:464-569):
+ * grad: n elements; out: n/W elements (out_dtype), rank r's partition sum. */
+int zpp_qgz_reduce_scatter(zpp_comm_t comm, size_t sym_offset, const void* grad, int dtype, int64_t n, int stages, int reorder,
+                           int intra_bits, int64_t intra_block, int inter_bits, int64_t inter_block, void* out,
+                           int out_dtype, void* errflag, void* stream);
+
+/* symmetric-workspace bytes each fused collective needs at its sym_offset
+ * (double-buffered; 256-byte aligned regions) */
+size_t zpp_qwz_sym_bytes(int64_t shard_len, int bits, int64_t block, int world);
+size_t zpp_qgz_sym_bytes(int64_t n, int world, int stages, int intra_bits, int64_t intra_block, int inter_bits,
+                         int64_t inter_block);
+size_t zpp_hpz_sym_bytes(int64_t sec_len, int elem_bytes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ZPP_H_ */

@@ -1,0 +1,436 @@
+// Host launchers + C ABI for the codec kernels (K0..K4).
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "zpp_internal.h"
+#include "zpp_kernels.cuh"
+
+namespace zpp {
+
+// ---------------------------------------------------------------------------
+// error plumbing
+
+static thread_local std::string g_last_error;
+
+int fail(int status, const std::string& msg) {
+  g_last_error = msg;
+  return status;
+}
+
+int check_cuda(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return ZPP_OK;
+  return fail(ZPP_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+int sm_count() {
+  static int cached = 0;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&cached, cudaDevAttrMultiProcessorCount, dev);
+    if (cached <= 0) cached = 148;
+  });
+  return cached;
+}
+
+// one resident wave of CTAs (persistent-style grid-stride), capped by work
+template <typename K>
+static int grid_for(K kernel, int threads, int64_t needed_ctas) {
+  static thread_local int dummy = 0;
+  (void)dummy;
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, 0) != cudaSuccess || occ <= 0) occ = 1;
+  int64_t g = (int64_t)sm_count() * occ;
+  if (needed_ctas < g) g = needed_ctas;
+  return (int)(g < 1 ? 1 : g);
+}
+
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+static size_t dtype_size(int dt) {
+  switch (dt) {
+    case ZPP_F32: return 4;
+    case ZPP_F16: return 2;
+    case ZPP_BF16: return 2;
+    case ZPP_F64: return 8;
+  }
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// K0 / K1
+
+template <typename T, int BITS, int LANES, int EPL, typename Addr>
+static int run_qreg(const T* x, const Addr& addr, int64_t n_blocks, uint8_t* codes, float* absmax, uint32_t* flag,
+                    cudaStream_t st) {
+  auto k = quantize_reg_kernel<T, BITS, LANES, EPL, true, Addr>;
+  const int teams_per_cta = 256 / LANES;
+  const int grid = grid_for(k, 256, ceil_div(n_blocks, teams_per_cta));
+  k<<<grid, 256, 0, st>>>(x, addr, n_blocks, codes, absmax, flag);
+  return check_cuda(cudaGetLastError(), "quantize_reg_kernel launch");
+}
+
+template <typename T, int BITS, typename Addr>
+static int dispatch_qreg(const T* x, const Addr& addr, int64_t n_blocks, int64_t block, uint8_t* codes,
+                         float* absmax, uint32_t* flag, cudaStream_t st, bool* handled) {
+  *handled = true;
+  switch (block) {
+    case 64: return run_qreg<T, BITS, 8, 8>(x, addr, n_blocks, codes, absmax, flag, st);
+    case 128: return run_qreg<T, BITS, 16, 8>(x, addr, n_blocks, codes, absmax, flag, st);
+    case 256: return run_qreg<T, BITS, 32, 8>(x, addr, n_blocks, codes, absmax, flag, st);
+    case 512: return run_qreg<T, BITS, 32, 16>(x, addr, n_blocks, codes, absmax, flag, st);
+    case 1024: return run_qreg<T, BITS, 32, 32>(x, addr, n_blocks, codes, absmax, flag, st);
+    case 2048: return run_qreg<T, BITS, 32, 64>(x, addr, n_blocks, codes, absmax, flag, st);
+  }
+  *handled = false;
+  return ZPP_OK;
+}
+
+template <typename T, int BITS, typename Addr>
+static int run_qgeneric(const T* x, const Addr& addr, int64_t n_out, int64_t block, uint8_t* codes, void* absmax,
+                        uint32_t* flag, cudaStream_t st) {
+  using Bits = typename GenTraits<T>::Bits;
+  const int64_t nb = ceil_div(n_out, block);
+  const int64_t n_chunks = nb * block / 8;
+  int rc = check_cuda(cudaMemsetAsync(absmax, 0, nb * sizeof(Bits), st), "absmax memset");
+  if (rc) return rc;
+  auto k1 = absmax_generic_kernel<T, Addr>;
+  const int g1 = grid_for(k1, 256, ceil_div(n_chunks, 256));
+  k1<<<g1, 256, 0, st>>>(x, addr, n_chunks, block, reinterpret_cast<Bits*>(absmax), flag);
+  rc = check_cuda(cudaGetLastError(), "absmax_generic_kernel launch");
+  if (rc) return rc;
+  auto k2 = quantize_generic_kernel<T, BITS, Addr>;
+  const int g2 = grid_for(k2, 256, ceil_div(n_chunks, 256));
+  k2<<<g2, 256, 0, st>>>(x, addr, n_chunks, block, reinterpret_cast<const Bits*>(absmax), codes);
+  return check_cuda(cudaGetLastError(), "quantize_generic_kernel launch");
+}
+
+template <typename T, int BITS, typename Addr>
+static int quantize_t(const void* xv, const Addr& addr, int64_t n_out, int64_t block, uint8_t* codes, void* absmax,
+                      uint32_t* flag, cudaStream_t st) {
+  const T* x = reinterpret_cast<const T*>(xv);
+  const int64_t nb = ceil_div(n_out, block);
+  if constexpr (!std::is_same<T, double>::value) {
+    if (aligned16(x)) {
+      bool handled = false;
+      int rc = dispatch_qreg<T, BITS>(x, addr, nb, block, codes, reinterpret_cast<float*>(absmax), flag, st,
+                                      &handled);
+      if (handled) return rc;
+    }
+  }
+  return run_qgeneric<T, BITS>(x, addr, n_out, block, codes, absmax, flag, st);
+}
+
+template <typename Addr>
+static int quantize_dispatch(const void* x, int dtype, const Addr& addr, int64_t n_out, int bits, int64_t block,
+                             uint8_t* codes, void* absmax, uint32_t* flag, cudaStream_t st) {
+#define ZPP_Q(T)                                                                            \
+  return bits == 8 ? quantize_t<T, 8>(x, addr, n_out, block, codes, absmax, flag, st)      \
+                   : quantize_t<T, 4>(x, addr, n_out, block, codes, absmax, flag, st);
+  switch (dtype) {
+    case ZPP_F32: ZPP_Q(float)
+    case ZPP_F16: ZPP_Q(__half)
+    case ZPP_BF16: ZPP_Q(__nv_bfloat16)
+    case ZPP_F64: ZPP_Q(double)
+  }
+#undef ZPP_Q
+  return fail(ZPP_ERR_VALIDATION, "unknown input dtype");
+}
+
+int launch_quantize(const void* x, int dtype, const AddrSpec& a, int64_t n_out, int bits, int64_t block,
+                    uint8_t* codes, void* absmax, uint32_t* flag, cudaStream_t st) {
+  if (n_out == 0) return ZPP_OK;
+  if (a.swizzle) {
+    SwizzleAddr addr{a.L, a.part, a.stage_off, a.X, a.Y, a.reorder};
+    return quantize_dispatch(x, dtype, addr, n_out, bits, block, codes, absmax, flag, st);
+  }
+  PlainAddr addr{a.n};
+  return quantize_dispatch(x, dtype, addr, n_out, bits, block, codes, absmax, flag, st);
+}
+
+// ---------------------------------------------------------------------------
+// K4 gather-dequantize and K3 dequant-reduce
+
+static int fill_table(SrcTable& t, const void* const* codes, const void* const* absmax, int n_src) {
+  if (n_src < 1 || n_src > kMaxSrc) return fail(ZPP_ERR_VALIDATION, "n_src must be in [1, 64]");
+  for (int i = 0; i < n_src; ++i) {
+    if (!codes[i] || !absmax[i]) return fail(ZPP_ERR_VALIDATION, "null source pointer");
+    t.codes[i] = reinterpret_cast<const uint8_t*>(codes[i]);
+    t.absmax[i] = absmax[i];
+  }
+  for (int i = n_src; i < kMaxSrc; ++i) {
+    t.codes[i] = nullptr;
+    t.absmax[i] = nullptr;
+  }
+  return ZPP_OK;
+}
+
+template <int BITS, typename A, typename O>
+static int run_gather(const SrcTable& t, int n_src, int rot, int64_t shard_len, int64_t block, void* out,
+                      void* sec_out, int64_t sec_lo, int64_t sec_len, uint32_t* flag, cudaStream_t st) {
+  auto k = dequant_gather_kernel<BITS, A, O>;
+  const int64_t groups = ceil_div(ceil_div(shard_len, 8), 32) * n_src;
+  const int grid = grid_for(k, 256, ceil_div(groups, 8));
+  const int vec_ok = aligned16(out) && (shard_len % 8 == 0);
+  k<<<grid, 256, 0, st>>>(t, n_src, rot, shard_len, block, reinterpret_cast<O*>(out), reinterpret_cast<O*>(sec_out),
+                          sec_lo, sec_len, vec_ok, flag);
+  return check_cuda(cudaGetLastError(), "dequant_gather_kernel launch");
+}
+
+template <int BITS, typename A, typename O>
+static int run_reduce(const SrcTable& t, int n_src, int64_t n, int64_t block, void* out, double post_scale,
+                      uint32_t* flag, cudaStream_t st) {
+  auto k = dequant_reduce_kernel<BITS, A, O>;
+  const int grid = grid_for(k, 256, ceil_div(ceil_div(n, 8), 256));
+  k<<<grid, 256, 0, st>>>(t, n_src, n, block, reinterpret_cast<O*>(out), post_scale, aligned16(out), flag);
+  return check_cuda(cudaGetLastError(), "dequant_reduce_kernel launch");
+}
+
+#define ZPP_DISPATCH_BA_O(FN, ...)                                                                  \
+  do {                                                                                              \
+    if (absmax_dtype != ZPP_F32 && absmax_dtype != ZPP_F64)                                         \
+      return fail(ZPP_ERR_VALIDATION, "absmax dtype must be F32 or F64");                           \
+    const bool a64 = absmax_dtype == ZPP_F64;                                                       \
+    switch (out_dtype) {                                                                            \
+      case ZPP_F32:                                                                                 \
+        if (bits == 8) return a64 ? FN<8, double, float>(__VA_ARGS__) : FN<8, float, float>(__VA_ARGS__); \
+        return a64 ? FN<4, double, float>(__VA_ARGS__) : FN<4, float, float>(__VA_ARGS__);          \
+      case ZPP_F16:                                                                                 \
+        if (bits == 8) return a64 ? FN<8, double, __half>(__VA_ARGS__) : FN<8, float, __half>(__VA_ARGS__); \
+        return a64 ? FN<4, double, __half>(__VA_ARGS__) : FN<4, float, __half>(__VA_ARGS__);        \
+      case ZPP_BF16:                                                                                \
+        if (bits == 8)                                                                              \
+          return a64 ? FN<8, double, __nv_bfloat16>(__VA_ARGS__) : FN<8, float, __nv_bfloat16>(__VA_ARGS__); \
+        return a64 ? FN<4, double, __nv_bfloat16>(__VA_ARGS__) : FN<4, float, __nv_bfloat16>(__VA_ARGS__); \
+      case ZPP_F64:                                                                                 \
+        if (bits == 8) return a64 ? FN<8, double, double>(__VA_ARGS__) : FN<8, float, double>(__VA_ARGS__); \
+        return a64 ? FN<4, double, double>(__VA_ARGS__) : FN<4, float, double>(__VA_ARGS__);        \
+    }                                                                                               \
+    return fail(ZPP_ERR_VALIDATION, "unknown output dtype");                                        \
+  } while (0)
+
+int launch_gather_dequant(const void* const* codes, const void* const* absmax, int absmax_dtype, int n_src, int rot,
+                          int64_t shard_len, int bits, int64_t block, void* out, int out_dtype, void* sec_out,
+                          int64_t sec_lo, int64_t sec_len, uint32_t* flag, cudaStream_t st) {
+  if (shard_len == 0) return ZPP_OK;
+  SrcTable t;
+  int rc = fill_table(t, codes, absmax, n_src);
+  if (rc) return rc;
+  rot = ((rot % n_src) + n_src) % n_src;
+  ZPP_DISPATCH_BA_O(run_gather, t, n_src, rot, shard_len, block, out, sec_out, sec_lo, sec_len, flag, st);
+}
+
+int launch_dequant_reduce(const void* const* codes, const void* const* absmax, int absmax_dtype, int n_src, int64_t n,
+                          int bits, int64_t block, void* out, int out_dtype, double post_scale, uint32_t* flag,
+                          cudaStream_t st) {
+  if (n == 0) return ZPP_OK;
+  SrcTable t;
+  int rc = fill_table(t, codes, absmax, n_src);
+  if (rc) return rc;
+  ZPP_DISPATCH_BA_O(run_reduce, t, n_src, n, block, out, post_scale, flag, st);
+}
+
+// ---------------------------------------------------------------------------
+// K2
+
+bool drq_has_reg_path(int64_t out_block) {
+  return out_block == 64 || out_block == 128 || out_block == 256 || out_block == 512 || out_block == 1024;
+}
+
+size_t drq_workspace_bytes(int64_t n, int64_t out_block) {
+  if (drq_has_reg_path(out_block)) return 0;
+  return (size_t)(ceil_div(n, out_block) * out_block) * sizeof(double);
+}
+
+template <int IBITS, typename IA, int OBITS, int LANES, int EPL>
+static int run_drq(const SrcTable& t, int n_src, int64_t n, int64_t in_block, int64_t nbo, uint8_t* codes,
+                   double* absmax, uint32_t* flag, cudaStream_t st) {
+  auto k = drq_reg_kernel<IBITS, IA, OBITS, LANES, EPL>;
+  const int grid = grid_for(k, 256, ceil_div(nbo, 256 / LANES));
+  k<<<grid, 256, 0, st>>>(t, n_src, n, in_block, nbo, codes, absmax, flag);
+  return check_cuda(cudaGetLastError(), "drq_reg_kernel launch");
+}
+
+template <int IBITS, typename IA, int OBITS>
+static int drq_block(const SrcTable& t, int n_src, int64_t n, int64_t in_block, int64_t out_block, uint8_t* codes,
+                     double* absmax, uint32_t* flag, cudaStream_t st) {
+  const int64_t nbo = ceil_div(n, out_block);
+  switch (out_block) {
+    case 64: return run_drq<IBITS, IA, OBITS, 8, 8>(t, n_src, n, in_block, nbo, codes, absmax, flag, st);
+    case 128: return run_drq<IBITS, IA, OBITS, 16, 8>(t, n_src, n, in_block, nbo, codes, absmax, flag, st);
+    case 256: return run_drq<IBITS, IA, OBITS, 32, 8>(t, n_src, n, in_block, nbo, codes, absmax, flag, st);
+    case 512: return run_drq<IBITS, IA, OBITS, 32, 16>(t, n_src, n, in_block, nbo, codes, absmax, flag, st);
+    case 1024: return run_drq<IBITS, IA, OBITS, 32, 32>(t, n_src, n, in_block, nbo, codes, absmax, flag, st);
+  }
+  return fail(ZPP_ERR_VALIDATION, "no register path for this output block");
+}
+
+int launch_drq(const void* const* codes, const void* const* absmax, int absmax_dtype, int n_src, int64_t n,
+               int in_bits, int64_t in_block, int out_bits, int64_t out_block, uint8_t* out_codes,
+               double* out_absmax, void* workspace, size_t ws_bytes, uint32_t* flag, cudaStream_t st) {
+  if (n == 0) return ZPP_OK;
+  SrcTable t;
+  int rc = fill_table(t, codes, absmax, n_src);
+  if (rc) return rc;
+  if (absmax_dtype != ZPP_F32 && absmax_dtype != ZPP_F64)
+    return fail(ZPP_ERR_VALIDATION, "absmax dtype must be F32 or F64");
+  const bool a64 = absmax_dtype == ZPP_F64;
+  if (drq_has_reg_path(out_block)) {
+#define ZPP_DRQ(IB, OB)                                                                                  \
+  return a64 ? drq_block<IB, double, OB>(t, n_src, n, in_block, out_block, out_codes, out_absmax, flag, st) \
+             : drq_block<IB, float, OB>(t, n_src, n, in_block, out_block, out_codes, out_absmax, flag, st);
+    if (in_bits == 8 && out_bits == 8) ZPP_DRQ(8, 8)
+    if (in_bits == 8 && out_bits == 4) ZPP_DRQ(8, 4)
+    if (in_bits == 4 && out_bits == 8) ZPP_DRQ(4, 8)
+    ZPP_DRQ(4, 4)
+#undef ZPP_DRQ
+  }
+  // generic: f64 fold into the workspace (K3 with f64 output), then the
+  // generic f64 quantizer -- identical arithmetic, three launches.
+  const size_t need = drq_workspace_bytes(n, out_block);
+  if (!workspace || ws_bytes < need) return fail(ZPP_ERR_VALIDATION, "workspace too small for fused requantize");
+  rc = launch_dequant_reduce(codes, absmax, absmax_dtype, n_src, n, in_bits, in_block, workspace, ZPP_F64, 1.0, flag,
+                             st);
+  if (rc) return rc;
+  AddrSpec a;
+  a.n = n;
+  return launch_quantize(workspace, ZPP_F64, a, n, out_bits, out_block, out_codes, out_absmax, flag, st);
+}
+
+}  // namespace zpp
+
+// ===========================================================================
+// C ABI
+
+using namespace zpp;
+
+static int check_cfg(int bits, int64_t block) {
+  if (bits != 4 && bits != 8) return fail(ZPP_ERR_CONFIG, "bit_width must be 4 or 8");
+  if (block < 8 || block % 8 != 0) return fail(ZPP_ERR_CONFIG, "block_size must be a positive multiple of 8");
+  return ZPP_OK;
+}
+
+static int check_dtype(int dt) {
+  if (dtype_size(dt) == 0) return fail(ZPP_ERR_VALIDATION, "unknown dtype");
+  return ZPP_OK;
+}
+
+extern "C" {
+
+int zpp_version(void) { return 10000; }
+
+const char* zpp_last_error(void) { return g_last_error.c_str(); }
+
+int zpp_device_sm_count(void) { return sm_count(); }
+
+int zpp_quantize(const void* x, int dtype, int64_t n, int bits, int64_t block, void* codes, void* absmax,
+                 void* errflag, void* stream) {
+  int rc = check_cfg(bits, block);
+  if (rc || (rc = check_dtype(dtype))) return rc;
+  if (n < 0) return fail(ZPP_ERR_VALIDATION, "negative length");
+  if (n > 0 && (!x || !codes || !absmax)) return fail(ZPP_ERR_VALIDATION, "null pointer");
+  AddrSpec a;
+  a.n = n;
+  return launch_quantize(x, dtype, a, n, bits, block, reinterpret_cast<uint8_t*>(codes), absmax,
+                         reinterpret_cast<uint32_t*>(errflag), reinterpret_cast<cudaStream_t>(stream));
+}
+
+int zpp_swizzle_quantize(const void* grad, int dtype, int64_t n, int X, int Y, int S, int stage, int reorder, int bits,
+                         int64_t block, void* codes, void* absmax, void* errflag, void* stream) {
+  int rc = check_cfg(bits, block);
+  if (rc || (rc = check_dtype(dtype))) return rc;
+  if (X < 1 || Y < 1 || S < 1) return fail(ZPP_ERR_VALIDATION, "X, Y, S must be >= 1");
+  if (stage < 0 || stage >= S) return fail(ZPP_ERR_VALIDATION, "stage out of range");
+  const int64_t T = (int64_t)X * Y;
+  if (n < 0 || n % (S * T)) return fail(ZPP_ERR_VALIDATION, "input length not divisible by stages*world");
+  const int64_t L = n / (S * T);
+  if (L % block) return fail(ZPP_ERR_VALIDATION, "slice length is not a multiple of block_size");
+  if (n > 0 && (!grad || !codes || !absmax)) return fail(ZPP_ERR_VALIDATION, "null pointer");
+  AddrSpec a;
+  a.swizzle = true;
+  a.L = L;
+  a.part = (int64_t)S * L;
+  a.stage_off = (int64_t)stage * L;
+  a.X = X;
+  a.Y = Y;
+  a.reorder = reorder ? 1 : 0;
+  return launch_quantize(grad, dtype, a, T * L, bits, block, reinterpret_cast<uint8_t*>(codes), absmax,
+                         reinterpret_cast<uint32_t*>(errflag), reinterpret_cast<cudaStream_t>(stream));
+}
+
+int zpp_dequantize(const void* codes, const void* absmax, int absmax_dtype, int64_t n, int bits, int64_t block,
+                   void* out, int out_dtype, void* errflag, void* stream) {
+  int rc = check_cfg(bits, block);
+  if (rc || (rc = check_dtype(out_dtype))) return rc;
+  if (n < 0) return fail(ZPP_ERR_VALIDATION, "negative length");
+  if (n == 0) return ZPP_OK;
+  if (!out) return fail(ZPP_ERR_VALIDATION, "null pointer");
+  const void* c[1] = {codes};
+  const void* a[1] = {absmax};
+  return launch_gather_dequant(c, a, absmax_dtype, 1, 0, n, bits, block, out, out_dtype, nullptr, 0, 0,
+                               reinterpret_cast<uint32_t*>(errflag), reinterpret_cast<cudaStream_t>(stream));
+}
+
+int zpp_gather_dequantize(const void* const* codes, const void* const* absmax, int absmax_dtype, int n_src, int rot,
+                          int64_t shard_len, int bits, int64_t block, void* out, int out_dtype, void* sec_out,
+                          int64_t sec_lo, int64_t sec_len, void* errflag, void* stream) {
+  int rc = check_cfg(bits, block);
+  if (rc || (rc = check_dtype(out_dtype))) return rc;
+  if (shard_len < 0 || !codes || !absmax) return fail(ZPP_ERR_VALIDATION, "bad arguments");
+  if (shard_len > 0 && !out) return fail(ZPP_ERR_VALIDATION, "null pointer");
+  return launch_gather_dequant(codes, absmax, absmax_dtype, n_src, rot, shard_len, bits, block, out, out_dtype,
+                               sec_out, sec_lo, sec_len, reinterpret_cast<uint32_t*>(errflag),
+                               reinterpret_cast<cudaStream_t>(stream));
+}
+
+int zpp_dequant_reduce(const void* const* codes, const void* const* absmax, int absmax_dtype, int n_src, int64_t n,
+                       int bits, int64_t block, void* out, int out_dtype, double post_scale, void* errflag,
+                       void* stream) {
+  int rc = check_cfg(bits, block);
+  if (rc || (rc = check_dtype(out_dtype))) return rc;
+  if (n < 0 || !codes || !absmax) return fail(ZPP_ERR_VALIDATION, "bad arguments");
+  if (n > 0 && !out) return fail(ZPP_ERR_VALIDATION, "null pointer");
+  return launch_dequant_reduce(codes, absmax, absmax_dtype, n_src, n, bits, block, out, out_dtype, post_scale,
+                               reinterpret_cast<uint32_t*>(errflag), reinterpret_cast<cudaStream_t>(stream));
+}
+
+int zpp_dequant_reduce_quant(const void* const* codes, const void* const* absmax, int absmax_dtype, int n_src,
+                             int64_t n, int in_bits, int64_t in_block, int out_bits, int64_t out_block,
+                             void* out_codes, void* out_absmax, void* workspace, size_t workspace_bytes,
+                             void* errflag, void* stream) {
+  int rc = check_cfg(in_bits, in_block);
+  if (rc || (rc = check_cfg(out_bits, out_block))) return rc;
+  if (n < 0 || !codes || !absmax) return fail(ZPP_ERR_VALIDATION, "bad arguments");
+  if (n > 0 && (!out_codes || !out_absmax)) return fail(ZPP_ERR_VALIDATION, "null pointer");
+  return launch_drq(codes, absmax, absmax_dtype, n_src, n, in_bits, in_block, out_bits, out_block,
+                    reinterpret_cast<uint8_t*>(out_codes), reinterpret_cast<double*>(out_absmax), workspace,
+                    workspace_bytes, reinterpret_cast<uint32_t*>(errflag), reinterpret_cast<cudaStream_t>(stream));
+}
+
+size_t zpp_drq_workspace_bytes(int64_t n, int64_t out_block) {
+  if (n <= 0 || out_block < 8) return 0;
+  return drq_workspace_bytes(n, out_block);
+}
+
+int zpp_scales(const void* absmax, int absmax_dtype, int64_t n_blocks, int bits, void* out_f64, void* stream) {
+  if (bits != 4 && bits != 8) return fail(ZPP_ERR_CONFIG, "bit_width must be 4 or 8");
+  if (n_blocks <= 0) return ZPP_OK;
+  if (!absmax || !out_f64) return fail(ZPP_ERR_VALIDATION, "null pointer");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int grid = (int)std::min<int64_t>(ceil_div(n_blocks, 256), 4 * sm_count());
+  double* o = reinterpret_cast<double*>(out_f64);
+  if (absmax_dtype == ZPP_F32) {
+    if (bits == 8) scales_kernel<8, float><<<grid, 256, 0, st>>>(reinterpret_cast<const float*>(absmax), n_blocks, o);
+    else scales_kernel<4, float><<<grid, 256, 0, st>>>(reinterpret_cast<const float*>(absmax), n_blocks, o);
+  } else if (absmax_dtype == ZPP_F64) {
+    if (bits == 8) scales_kernel<8, double><<<grid, 256, 0, st>>>(reinterpret_cast<const double*>(absmax), n_blocks, o);
+    else scales_kernel<4, double><<<grid, 256, 0, st>>>(reinterpret_cast<const double*>(absmax), n_blocks, o);
+  } else {
+    return fail(ZPP_ERR_VALIDATION, "absmax dtype must be F32 or F64");
+  }
+  return check_cuda(cudaGetLastError(), "scales_kernel launch");
+}
+
+}  // extern "C"

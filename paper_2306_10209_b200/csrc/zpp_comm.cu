@@ -1,0 +1,394 @@
+// Multi-GPU layer: one process per GPU, a symmetric device workspace mapped by
+// every rank through CUDA IPC, device-side barriers on flag words in that
+// workspace, and the three ZeRO++ collectives fused with their codec kernels
+// over NVLink peer loads (no staging copies, no NCCL on the data path).
+//
+//   qwZ  zs/collectives.py:244-282   K0 -> world barrier -> K4 pulling peers' codes
+//   hpZ  zs/collectives.py:202-241   (groups) group barrier -> peer copy of the
+//                                    secondary shards held in HBM
+//   qgZ  zs/collectives.py:464-569   per stage: K1 -> group barrier -> K2 pulling
+//                                    the X intra messages -> cross barrier -> K3
+//                                    pulling the Y hop-2 segments
+//
+// Double buffering: every use of a region alternates between two halves, and a
+// rank only rewrites a half after passing a barrier that every reader of the
+// previous contents must have reached after finishing its reads.
+#include <cstring>
+#include <vector>
+
+#include "zpp_internal.h"
+#include "zpp_kernels.cuh"
+
+using namespace zpp;
+
+namespace {
+
+constexpr int kMaxRanks = kMaxSrc;
+constexpr int kScopes = 3;  // world, group, cross
+constexpr size_t kFlagBytes = kScopes * kMaxRanks * sizeof(uint32_t);
+
+inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+struct BarrierArgs {
+  uint32_t* remote[kMaxRanks];  // flag slot this rank writes in member m's buffer
+  const uint32_t* local[kMaxRanks];  // flag slot member m writes in my buffer
+};
+
+__global__ void barrier_kernel(BarrierArgs a, int n, uint32_t epoch, uint64_t timeout_ns, uint32_t* flag) {
+  const int t = threadIdx.x;
+  __threadfence_system();
+  __syncthreads();
+  if (t < n) {
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(a.remote[t]), "r"(epoch) : "memory");
+  }
+  if (t < n) {
+    const uint64_t t0 = globaltimer_ns();
+    uint32_t v = 0;
+    while (true) {
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(a.local[t]) : "memory");
+      if ((int32_t)(v - epoch) >= 0) break;
+      if (globaltimer_ns() - t0 > timeout_ns) {
+        raise_flag(flag, FLAG_TIMEOUT);
+        break;
+      }
+      __nanosleep(64);
+    }
+  }
+  __syncthreads();
+  __threadfence_system();
+}
+
+// byte copy of n_src peer segments into out (hpZ gather), 16 B vectors when aligned
+__global__ void __launch_bounds__(256)
+gather_copy_kernel(SrcTable src, int n_src, int rot, int64_t seg_bytes, uint8_t* __restrict__ out, int vec) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarp = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  if (vec) {
+    const int64_t units = seg_bytes / 16;
+    const int64_t groups = (units + 31) / 32;
+    for (int64_t g = gwarp; g < groups * n_src; g += nwarp) {
+      const int s = (int)((g % n_src + rot) % n_src);
+      const int64_t u = (g / n_src) * 32 + lane;
+      if (u < units) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(src.codes[s]) + u);
+        reinterpret_cast<uint4*>(out + s * seg_bytes)[u] = v;
+      }
+    }
+  } else {
+    const int64_t total = seg_bytes * n_src;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
+      const int s = (int)(i / seg_bytes);
+      out[i] = src.codes[s][i - s * seg_bytes];
+    }
+  }
+}
+
+}  // namespace
+
+struct zpp_comm {
+  int rank = 0, world = 1, group = 1;
+  size_t sym_bytes = 0;
+  uint8_t* local = nullptr;        // this rank's symmetric buffer (sym_bytes + flags)
+  uint8_t* peers[kMaxRanks] = {};  // every rank's buffer in this address space
+  bool opened[kMaxRanks] = {};
+  uint32_t epoch[kScopes] = {};
+  uint64_t qwz_uses = 0, qgz_uses = 0;
+  cudaIpcMemHandle_t handle;
+  int device = 0;
+
+  uint32_t* flag_slot(int owner, int scope, int writer) {
+    return reinterpret_cast<uint32_t*>(peers[owner] + sym_bytes) + scope * kMaxRanks + writer;
+  }
+  // members of a barrier scope, ascending
+  std::vector<int> members(int scope) const {
+    std::vector<int> m;
+    const int node = rank / group, loc = rank % group;
+    if (scope == 0) {
+      for (int r = 0; r < world; ++r) m.push_back(r);
+    } else if (scope == 1) {
+      for (int j = 0; j < group; ++j) m.push_back(node * group + j);
+    } else {
+      for (int c = 0; c < world / group; ++c) m.push_back(c * group + loc);
+    }
+    return m;
+  }
+};
+
+static int comm_ok(zpp_comm_t c) {
+  if (!c) return fail(ZPP_ERR_VALIDATION, "null communicator");
+  for (int r = 0; r < c->world; ++r)
+    if (!c->peers[r]) return fail(ZPP_ERR_COMM, "peers not opened (call zpp_comm_open_peers)");
+  return ZPP_OK;
+}
+
+static int barrier(zpp_comm_t c, int scope, int timeout_ms, uint32_t* flag, cudaStream_t st) {
+  std::vector<int> m = c->members(scope);
+  const uint32_t e = ++c->epoch[scope];
+  BarrierArgs a;
+  for (size_t i = 0; i < m.size(); ++i) {
+    a.remote[i] = c->flag_slot(m[i], scope, c->rank);
+    a.local[i] = c->flag_slot(c->rank, scope, m[i]);
+  }
+  const uint64_t to = (uint64_t)(timeout_ms > 0 ? timeout_ms : 60000) * 1000000ull;
+  barrier_kernel<<<1, 64, 0, st>>>(a, (int)m.size(), e, to, flag);
+  return check_cuda(cudaGetLastError(), "barrier_kernel launch");
+}
+
+static size_t absmax_elem(int dtype) { return dtype == ZPP_F64 ? 8 : 4; }
+static const int kBarrierTimeoutMs = 60000;
+
+extern "C" {
+
+int zpp_comm_create(int rank, int world, int group_size, size_t sym_bytes, zpp_comm_t* out) {
+  if (!out) return fail(ZPP_ERR_VALIDATION, "null output");
+  if (world < 1 || world > kMaxRanks) return fail(ZPP_ERR_VALIDATION, "world must be in [1, 64]");
+  if (rank < 0 || rank >= world) return fail(ZPP_ERR_VALIDATION, "rank out of range");
+  if (group_size < 1 || world % group_size) return fail(ZPP_ERR_VALIDATION, "group_size must divide world");
+  zpp_comm* c = new zpp_comm();
+  c->rank = rank;
+  c->world = world;
+  c->group = group_size;
+  c->sym_bytes = align256(sym_bytes);
+  cudaGetDevice(&c->device);
+  int rc = check_cuda(cudaMalloc(&c->local, c->sym_bytes + kFlagBytes), "cudaMalloc symmetric buffer");
+  if (rc) {
+    delete c;
+    return rc;
+  }
+  rc = check_cuda(cudaMemset(c->local + c->sym_bytes, 0, kFlagBytes), "flag memset");
+  if (!rc) rc = check_cuda(cudaIpcGetMemHandle(&c->handle, c->local), "cudaIpcGetMemHandle");
+  if (rc) {
+    cudaFree(c->local);
+    delete c;
+    return rc;
+  }
+  c->peers[rank] = c->local;
+  *out = c;
+  return ZPP_OK;
+}
+
+int zpp_comm_ipc_handle(zpp_comm_t c, void* handle_out) {
+  if (!c || !handle_out) return fail(ZPP_ERR_VALIDATION, "null argument");
+  static_assert(sizeof(cudaIpcMemHandle_t) == ZPP_IPC_HANDLE_BYTES, "IPC handle size");
+  std::memcpy(handle_out, &c->handle, sizeof(c->handle));
+  return ZPP_OK;
+}
+
+int zpp_comm_open_peers(zpp_comm_t c, const void* all_handles) {
+  if (!c || !all_handles) return fail(ZPP_ERR_VALIDATION, "null argument");
+  const uint8_t* h = reinterpret_cast<const uint8_t*>(all_handles);
+  for (int r = 0; r < c->world; ++r) {
+    if (r == c->rank || c->peers[r]) continue;
+    cudaIpcMemHandle_t hh;
+    std::memcpy(&hh, h + (size_t)r * ZPP_IPC_HANDLE_BYTES, sizeof(hh));
+    void* p = nullptr;
+    int rc = check_cuda(cudaIpcOpenMemHandle(&p, hh, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+    if (rc) return rc;
+    c->peers[r] = reinterpret_cast<uint8_t*>(p);
+    c->opened[r] = true;
+  }
+  return ZPP_OK;
+}
+
+void* zpp_comm_sym_ptr(zpp_comm_t c, int rank) {
+  if (!c || rank < 0 || rank >= c->world) return nullptr;
+  return c->peers[rank];
+}
+
+size_t zpp_comm_sym_bytes(zpp_comm_t c) { return c ? c->sym_bytes : 0; }
+
+int zpp_comm_barrier(zpp_comm_t c, int scope, int timeout_ms, void* errflag, void* stream) {
+  int rc = comm_ok(c);
+  if (rc) return rc;
+  if (scope < 0 || scope >= kScopes) return fail(ZPP_ERR_VALIDATION, "scope must be 0, 1 or 2");
+  return barrier(c, scope, timeout_ms, reinterpret_cast<uint32_t*>(errflag), reinterpret_cast<cudaStream_t>(stream));
+}
+
+int zpp_comm_destroy(zpp_comm_t c) {
+  if (!c) return ZPP_OK;
+  cudaDeviceSynchronize();
+  for (int r = 0; r < c->world; ++r)
+    if (c->opened[r]) cudaIpcCloseMemHandle(c->peers[r]);
+  cudaFree(c->local);
+  delete c;
+  return ZPP_OK;
+}
+
+// ---------------------------------------------------------------------------
+// qwZ
+
+static size_t qwz_region(int64_t shard_len, int bits, int64_t block, int dtype) {
+  const int64_t nb = ceil_div(shard_len, block);
+  return align256((size_t)code_bytes(shard_len, bits, block)) + align256((size_t)nb * absmax_elem(dtype));
+}
+
+size_t zpp_qwz_sym_bytes(int64_t shard_len, int bits, int64_t block, int world) {
+  (void)world;
+  return 2 * qwz_region(shard_len, bits, block, ZPP_F64);
+}
+
+int zpp_qwz_allgather(zpp_comm_t c, size_t sym_offset, const void* shard, int dtype, int64_t shard_len, int bits,
+                      int64_t block, void* out, int out_dtype, void* sec_out, int64_t sec_lo, int64_t sec_len,
+                      void* errflag, void* stream) {
+  int rc = comm_ok(c);
+  if (rc) return rc;
+  if ((bits != 4 && bits != 8) || block < 8 || block % 8) return fail(ZPP_ERR_CONFIG, "bad quant config");
+  if (shard_len < 0 || (shard_len > 0 && (!shard || !out))) return fail(ZPP_ERR_VALIDATION, "bad arguments");
+  if (dtype < 0 || dtype > ZPP_F64 || out_dtype < 0 || out_dtype > ZPP_F64)
+    return fail(ZPP_ERR_VALIDATION, "unknown dtype");
+  const size_t region = qwz_region(shard_len, bits, block, ZPP_F64);
+  if (sym_offset + 2 * region > c->sym_bytes) return fail(ZPP_ERR_VALIDATION, "symmetric buffer too small for qwZ");
+  if (shard_len == 0) return ZPP_OK;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  uint32_t* flag = reinterpret_cast<uint32_t*>(errflag);
+  const size_t base = sym_offset + (c->qwz_uses++ & 1) * region;
+  const size_t abs_off = align256((size_t)code_bytes(shard_len, bits, block));
+  AddrSpec a;
+  a.n = shard_len;
+  rc = launch_quantize(shard, dtype, a, shard_len, bits, block, c->local + base,
+                       c->local + base + abs_off, flag, st);
+  if (rc) return rc;
+  rc = barrier(c, 0, kBarrierTimeoutMs, flag, st);
+  if (rc) return rc;
+  const void* codes[kMaxRanks];
+  const void* absmax[kMaxRanks];
+  for (int r = 0; r < c->world; ++r) {
+    codes[r] = c->peers[r] + base;
+    absmax[r] = c->peers[r] + base + abs_off;
+  }
+  return launch_gather_dequant(codes, absmax, dtype == ZPP_F64 ? ZPP_F64 : ZPP_F32, c->world, c->rank, shard_len,
+                               bits, block, out, out_dtype, sec_out, sec_lo, sec_len, flag, st);
+}
+
+// ---------------------------------------------------------------------------
+// hpZ
+
+size_t zpp_hpz_sym_bytes(int64_t sec_len, int elem_bytes) { return align256((size_t)sec_len * elem_bytes); }
+
+int zpp_hpz_allgather(zpp_comm_t c, size_t sym_offset, int64_t sec_len, int elem_bytes, void* out, void* errflag,
+                      void* stream) {
+  int rc = comm_ok(c);
+  if (rc) return rc;
+  if (sec_len < 0 || elem_bytes <= 0 || (sec_len > 0 && !out)) return fail(ZPP_ERR_VALIDATION, "bad arguments");
+  const int64_t seg = sec_len * elem_bytes;
+  if (sym_offset + (size_t)seg > c->sym_bytes) return fail(ZPP_ERR_VALIDATION, "symmetric buffer too small for hpZ");
+  if (seg == 0) return ZPP_OK;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  rc = barrier(c, 1, kBarrierTimeoutMs, reinterpret_cast<uint32_t*>(errflag), st);
+  if (rc) return rc;
+  std::vector<int> m = c->members(1);
+  SrcTable t;
+  std::memset(&t, 0, sizeof(t));
+  for (size_t i = 0; i < m.size(); ++i) t.codes[i] = c->peers[m[i]] + sym_offset;
+  const int vec = (seg % 16 == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0) && (sym_offset % 16 == 0);
+  const int n = (int)m.size();
+  const int grid = (int)std::min<int64_t>(4 * sm_count(), std::max<int64_t>(1, ceil_div(seg * n, 16 * 256)));
+  gather_copy_kernel<<<grid, 256, 0, st>>>(t, n, c->rank % c->group, seg, reinterpret_cast<uint8_t*>(out), vec);
+  return check_cuda(cudaGetLastError(), "gather_copy_kernel launch");
+}
+
+// ---------------------------------------------------------------------------
+// qgZ
+
+struct QgzLayout {
+  int64_t L;
+  size_t send_codes, send_abs, hop_codes, hop_abs, ws, region;
+};
+
+static QgzLayout qgz_layout(int64_t n, int world, int Y, int stages, int ib, int64_t iblk, int ob, int64_t oblk) {
+  QgzLayout l;
+  l.L = n / ((int64_t)stages * world);
+  const int64_t send_elems = (int64_t)world * l.L;
+  const int64_t hop_elems = (int64_t)Y * l.L;
+  size_t off = 0;
+  l.send_codes = off;
+  off += align256((size_t)code_bytes(send_elems, ib, iblk));
+  l.send_abs = off;
+  off += align256((size_t)ceil_div(send_elems, iblk) * 8);
+  l.hop_codes = off;
+  off += align256((size_t)code_bytes(hop_elems, ob, oblk));
+  l.hop_abs = off;
+  off += align256((size_t)ceil_div(hop_elems, oblk) * 8);
+  l.ws = off;
+  off += align256(drq_workspace_bytes(hop_elems, oblk));
+  l.region = off;
+  return l;
+}
+
+size_t zpp_qgz_sym_bytes(int64_t n, int world, int stages, int intra_bits, int64_t intra_block, int inter_bits,
+                         int64_t inter_block) {
+  if (world < 1 || stages < 1 || intra_block < 8 || inter_block < 8) return 0;
+  return 2 * qgz_layout(n, world, world, stages, intra_bits, intra_block, inter_bits, inter_block).region;
+}
+
+int zpp_qgz_reduce_scatter(zpp_comm_t c, size_t sym_offset, const void* grad, int dtype, int64_t n, int stages,
+                           int reorder, int intra_bits, int64_t intra_block, int inter_bits, int64_t inter_block,
+                           void* out, int out_dtype, void* errflag, void* stream) {
+  int rc = comm_ok(c);
+  if (rc) return rc;
+  if ((intra_bits != 4 && intra_bits != 8) || (inter_bits != 4 && inter_bits != 8) || intra_block < 8 ||
+      intra_block % 8 || inter_block < 8 || inter_block % 8)
+    return fail(ZPP_ERR_CONFIG, "bad quant config");
+  if (stages < 1) return fail(ZPP_ERR_VALIDATION, "stages must be >= 1");
+  const int W = c->world, X = c->group, Y = W / X;
+  if (n < 0 || n % ((int64_t)stages * W)) return fail(ZPP_ERR_VALIDATION, "input length not divisible by stages*world");
+  const QgzLayout l = qgz_layout(n, W, Y, stages, intra_bits, intra_block, inter_bits, inter_block);
+  if (l.L % intra_block || l.L % inter_block)
+    return fail(ZPP_ERR_VALIDATION, "slice length is not a multiple of block_size");
+  if (sym_offset + 2 * l.region > c->sym_bytes) return fail(ZPP_ERR_VALIDATION, "symmetric buffer too small for qgZ");
+  if (n == 0) return ZPP_OK;
+  if (!grad || !out) return fail(ZPP_ERR_VALIDATION, "null pointer");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  uint32_t* flag = reinterpret_cast<uint32_t*>(errflag);
+  const int node = c->rank / X, loc = c->rank % X;
+  const int in_abs = dtype == ZPP_F64 ? ZPP_F64 : ZPP_F32;
+  const size_t in_abs_sz = absmax_elem(in_abs);
+  const size_t out_esz = out_dtype == ZPP_F64 ? 8 : (out_dtype == ZPP_F32 ? 4 : 2);
+  const int64_t L = l.L;
+  const int64_t msg_elems = (int64_t)Y * L;  // one hop-1 message
+  for (int s = 0; s < stages; ++s) {
+    const size_t base = sym_offset + (c->qgz_uses++ & 1) * l.region;
+    // K1: swizzle + quantize this stage's slices into my send buffer [j][c][e]
+    AddrSpec a;
+    a.swizzle = true;
+    a.L = L;
+    a.part = (int64_t)stages * L;
+    a.stage_off = (int64_t)s * L;
+    a.X = X;
+    a.Y = Y;
+    a.reorder = reorder ? 1 : 0;
+    rc = launch_quantize(grad, dtype, a, (int64_t)W * L, intra_bits, intra_block, c->local + base + l.send_codes,
+                         c->local + base + l.send_abs, flag, st);
+    if (rc) return rc;
+    rc = barrier(c, 1, kBarrierTimeoutMs, flag, st);
+    if (rc) return rc;
+    // K2: pull message `loc` from every group member (ascending local rank)
+    const void* codes[kMaxRanks];
+    const void* absmax[kMaxRanks];
+    for (int j = 0; j < X; ++j) {
+      const uint8_t* p = c->peers[node * X + j] + base;
+      codes[j] = p + l.send_codes + (size_t)code_bytes(msg_elems, intra_bits, intra_block) * loc;
+      absmax[j] = p + l.send_abs + (size_t)(msg_elems / intra_block) * in_abs_sz * loc;
+    }
+    rc = launch_drq(codes, absmax, in_abs, X, msg_elems, intra_bits, intra_block, inter_bits, inter_block,
+                    c->local + base + l.hop_codes, reinterpret_cast<double*>(c->local + base + l.hop_abs),
+                    c->local + base + l.ws, drq_workspace_bytes(msg_elems, inter_block), flag, st);
+    if (rc) return rc;
+    rc = barrier(c, 2, kBarrierTimeoutMs, flag, st);
+    if (rc) return rc;
+    // K3: pull segment `node` from the rank with my local index in every group
+    for (int g = 0; g < Y; ++g) {
+      const uint8_t* p = c->peers[g * X + loc] + base;
+      codes[g] = p + l.hop_codes + (size_t)code_bytes(L, inter_bits, inter_block) * node;
+      absmax[g] = p + l.hop_abs + (size_t)(L / inter_block) * 8 * node;
+    }
+    rc = launch_dequant_reduce(codes, absmax, ZPP_F64, Y, L, inter_bits, inter_block,
+                               reinterpret_cast<uint8_t*>(out) + (size_t)s * L * out_esz, out_dtype, 1.0, flag, st);
+    if (rc) return rc;
+  }
+  return ZPP_OK;
+}
+
+}  // extern "C"

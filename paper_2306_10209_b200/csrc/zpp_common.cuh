@@ -1,0 +1,173 @@
+// Shared device helpers for the ZeRO++ codec kernels (sm_100a).
+//
+// Numerics contract (reference: zs/quantizer.py:204-258):
+//   scale = f64(absmax) / qmax,  inv = qmax / f64(absmax) (0 if absmax == 0)
+//   code  = clip(rint_even(f64(x) * inv), -qmax, qmax)
+//   value = f64(code) * scale ; reductions fold in f64 from +0.0, ascending source.
+// Every operation below is an explicit _rn intrinsic or an exactness-preserving
+// integer trick, so nvcc can neither contract nor reorder them.
+#pragma once
+
+#include <cstdint>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+namespace zpp {
+
+enum DType : int { F32 = 0, F16 = 1, BF16 = 2, F64 = 3 };
+
+enum Flag : uint32_t {
+  FLAG_NONFINITE = 1u,  // non-finite input value (reference: ValidationError)
+  FLAG_BADCODE = 2u,    // code outside the symmetric range (reference: IntegrityError)
+  FLAG_TIMEOUT = 4u,    // a peer never arrived at a device barrier
+};
+
+__device__ __forceinline__ void raise_flag(uint32_t* flag, uint32_t bit) {
+  if (flag) atomicOr(flag, bit);
+}
+
+// ---------------------------------------------------------------------------
+// exact helpers
+
+// f64 division by the constant qmax (127 or 7), correctly rounded.
+// q0 = RN(m * RN(1/Q)); e = m - q0*Q (exact through FMA); RN(q0 + e * RN(1/Q))
+// is the correctly rounded quotient for normal m (Markstein); verified against
+// __ddiv_rn on every positive fp32 value and 2^30 random doubles in
+// tests/test_gpu_numerics.py.
+template <int Q>
+__device__ __forceinline__ double div_q(double m) {
+  constexpr double r = 1.0 / Q;
+  if (m < 1e-290) return __ddiv_rn(m, (double)Q);  // keep the proof's no-underflow premise
+  double q0 = __dmul_rn(m, r);
+  double e = __fma_rn(-q0, (double)Q, m);
+  return __fma_rn(e, r, q0);
+}
+
+// int code c in [-128, 127] given as the byte (c + 128) -> exact double c.
+// 2^52 + 2^51 has an all-zero low word, so OR-ing an unsigned value u < 2^31
+// into it gives exactly 2^52 + 2^51 + u; one exact subtraction recovers u - bias.
+__device__ __forceinline__ double biased_to_f64(uint32_t u, double magic_plus_bias) {
+  return __dsub_rn(__hiloint2double(0x43380000, (int)u), magic_plus_bias);
+}
+constexpr double kMagic52 = 6755399441055744.0;  // 2^52 + 2^51
+
+// round-half-even of a double to int via the 2^52+2^51 trick (|t| < 2^31).
+__device__ __forceinline__ int rint_f64(double t) {
+  return __double2loint(__dadd_rn(t, kMagic52));
+}
+
+// fp32 fast path: t = x * inv32, r = rint(t).  |t - t64| < 1.6e-5 where
+// t64 = RN64(x * inv64) (inv32 = RN32(inv64); two fp32 roundings of a value
+// <= qmax + 1e-5), so r == rint(t64) unless t lies within 2^-15 of a half
+// integer.  Those (rare) elements are redone in f64.
+constexpr float kMagic23 = 12582912.0f;  // 1.5 * 2^23
+constexpr float kTieGuard = 0.5f - 3.0517578125e-05f;
+
+// returns the float whose low byte is the two's complement code
+__device__ __forceinline__ uint32_t q_fast(float x, float inv32, bool& redo) {
+  float t = __fmul_rn(x, inv32);
+  float tm = __fadd_rn(t, kMagic23);
+  float r = __fsub_rn(tm, kMagic23);
+  float d = fabsf(__fsub_rn(t, r));
+  redo |= d > kTieGuard;
+  return __float_as_uint(tm);
+}
+
+template <int QMAX>
+__device__ __forceinline__ uint32_t q_exact(double x, double inv64) {
+  int k = rint_f64(__dmul_rn(x, inv64));
+  k = k > QMAX ? QMAX : (k < -QMAX ? -QMAX : k);
+  return (uint32_t)k;
+}
+
+// ---------------------------------------------------------------------------
+// packing: 8 codes (low byte of each word = two's complement code)
+
+__device__ __forceinline__ uint2 pack8_int8(const uint32_t (&b)[8]) {
+  uint32_t lo = __byte_perm(__byte_perm(b[0], b[1], 0x0040), __byte_perm(b[2], b[3], 0x0040), 0x5410);
+  uint32_t hi = __byte_perm(__byte_perm(b[4], b[5], 0x0040), __byte_perm(b[6], b[7], 0x0040), 0x5410);
+  return make_uint2(lo, hi);
+}
+
+// byte i = (c[2i] & 0xF) | (c[2i+1] & 0xF) << 4   (zs/quantizer.py:188-189)
+__device__ __forceinline__ uint32_t pack8_int4(const uint32_t (&b)[8]) {
+  uint32_t ev = __byte_perm(__byte_perm(b[0], b[2], 0x0040), __byte_perm(b[4], b[6], 0x0040), 0x5410);
+  uint32_t od = __byte_perm(__byte_perm(b[1], b[3], 0x0040), __byte_perm(b[5], b[7], 0x0040), 0x5410);
+  return (ev & 0x0F0F0F0Fu) | ((od << 4) & 0xF0F0F0F0u);
+}
+
+// ---------------------------------------------------------------------------
+// unpacking: codes -> biased unsigned (c + 128 for INT8, c + 8 for INT4) and
+// validity (the reference rejects -128 / -8, zs/quantizer.py:233-235)
+
+__device__ __forceinline__ bool has_byte_0x80(uint32_t w) {
+  uint32_t v = w ^ 0x80808080u;  // zero byte <=> code == -128
+  return ((v - 0x01010101u) & ~v & 0x80808080u) != 0;
+}
+__device__ __forceinline__ bool has_nibble_8(uint32_t w) {
+  uint32_t v = w ^ 0x88888888u;  // zero nibble <=> code == -8
+  return ((v - 0x11111111u) & ~v & 0x88888888u) != 0;
+}
+
+// 4 INT8 codes in w -> biased bytes u[i] = code_i + 128
+__device__ __forceinline__ void unpack4_int8(uint32_t w, uint32_t (&u)[4]) {
+  uint32_t f = w ^ 0x80808080u;
+  u[0] = __byte_perm(f, 0, 0x4440);
+  u[1] = __byte_perm(f, 0, 0x4441);
+  u[2] = __byte_perm(f, 0, 0x4442);
+  u[3] = __byte_perm(f, 0, 0x4443);
+}
+// 8 INT4 codes in w (low nibble first) -> biased nibbles code_i + 8
+__device__ __forceinline__ void unpack8_int4(uint32_t w, uint32_t (&u)[8]) {
+  uint32_t f = w ^ 0x88888888u;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) u[i] = (f >> (4 * i)) & 0xFu;
+}
+
+// ---------------------------------------------------------------------------
+// element types
+
+template <typename T> struct Elem;
+template <> struct Elem<float> {
+  static constexpr int kRawWords = 8;  // 32 bytes per 8 elements
+  static constexpr uint32_t kInfBits = 0x7f800000u;
+  __device__ static float to_float(uint32_t w, int /*half*/) { return __uint_as_float(w); }
+};
+
+template <int BITS> struct Codes {
+  static constexpr int kQmax = (1 << (BITS - 1)) - 1;
+  static constexpr int kBytesPer8 = BITS;  // 8 elements -> 8 or 4 bytes
+};
+
+// output conversion from an exact double
+template <typename O> __device__ __forceinline__ O from_f64(double v);
+template <> __device__ __forceinline__ float from_f64<float>(double v) { return __double2float_rn(v); }
+template <> __device__ __forceinline__ double from_f64<double>(double v) { return v; }
+template <> __device__ __forceinline__ __half from_f64<__half>(double v) { return __double2half(v); }
+template <> __device__ __forceinline__ __nv_bfloat16 from_f64<__nv_bfloat16>(double v) {
+  return __double2bfloat16(v);
+}
+
+// absmax storage: fp32 (exact for fp16/bf16/fp32 inputs) or f64
+template <typename A> __device__ __forceinline__ double absmax_f64(const A* p, int64_t i);
+template <> __device__ __forceinline__ double absmax_f64<float>(const float* p, int64_t i) {
+  return (double)__ldg(p + i);
+}
+template <> __device__ __forceinline__ double absmax_f64<double>(const double* p, int64_t i) {
+  return __ldg(p + i);
+}
+
+template <int BITS>
+__device__ __forceinline__ double scale_of(double m) {
+  return div_q<Codes<BITS>::kQmax>(m);
+}
+
+// global timer for bounded spins
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+}  // namespace zpp

@@ -1,0 +1,256 @@
+"""GPU parity of the codec kernels (K0 quantize, K4 dequantize, K2 fused,
+K3 reduce) against the reference's golden vectors and the CPU oracle.
+
+Bar: codes and scales bit-exact; every dequantized / reduced element equal to
+the reference's f64 value rounded once to the output dtype (bit-exact for
+f64)."""
+
+import numpy as np
+import pytest
+import torch
+
+import golden_util as gu
+from oracle import zpp_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+Q, M = gu.load("quant")
+
+
+def _zpp():
+    import paper_2306_10209_b200 as zpp
+    return zpp
+
+
+@pytest.mark.parametrize("case", range(len(M)))
+def test_quantize_golden(case):
+    zpp = _zpp()
+    m = M[case]
+    x = gu.to_torch(Q[f"{case}_input"], m["dtype"])
+    cfg = zpp.QuantConfig(bit_width=m["bits"], block_size=m["block"], mode=m["mode"])
+    q = zpp.quantize(x, cfg)
+    assert q.config.block_size == m["eff_block"]
+    assert np.array_equal(q.codes.cpu().numpy(), Q[f"{case}_codes"]), m["name"]
+    assert np.array_equal(q.scales.cpu().numpy(), Q[f"{case}_scales"]), m["name"]
+    assert (q.payload_bytes, q.metadata_bytes, q.padding_bytes, q.wire_bytes) == (
+        m["payload"], m["metadata"], m["padding"], m["wire"])
+    ref = Q[f"{case}_deq"]
+    for dt, name in [(torch.float64, "f64"), (torch.float32, "fp32"), (torch.float16, "fp16"),
+                     (torch.bfloat16, "bf16")]:
+        got = zpp.dequantize(q, dt).values.to(torch.float64).cpu().numpy()
+        want = gu.round_to(ref, name)
+        assert np.array_equal(got, want), (m["name"], name)
+
+
+def test_known_answers():
+    zpp = _zpp()
+    q = zpp.quantize(torch.tensor([1.0, -1.0, 0.5, -0.5], dtype=torch.float64, device="cuda"),
+                     zpp.QuantConfig(bit_width=8, block_size=8))
+    assert q.scales.cpu().tolist() == [1.0 / 127.0]
+    assert q.codes.cpu().numpy().view(np.int8)[:4].tolist() == [127, -127, 64, -64]
+    back = zpp.dequantize(q).values.cpu().numpy()
+    assert back[2] == np.float64(64) / np.float64(127)
+    q = zpp.quantize(torch.zeros(16, device="cuda"), zpp.QuantConfig(bit_width=4, block_size=8))
+    assert q.scales.cpu().tolist() == [0.0, 0.0] and not q.codes.any()
+
+
+def test_errors_map_to_reference_exceptions():
+    zpp = _zpp()
+    for bad in (float("nan"), float("inf"), -float("inf")):
+        for dt in (torch.float32, torch.float16, torch.bfloat16, torch.float64):
+            x = torch.ones(3000, dtype=dt, device="cuda")
+            x[1234] = bad
+            with pytest.raises(zpp.ValidationError):
+                zpp.quantize(x, zpp.QuantConfig(bit_width=8, block_size=2048))
+            with pytest.raises(zpp.ValidationError):
+                zpp.quantize(x, zpp.QuantConfig(bit_width=4, block_size=24))
+    q = zpp.quantize(torch.ones(8, device="cuda"), zpp.QuantConfig(bit_width=8, block_size=8))
+    q.codes[0] = 0x80
+    with pytest.raises(zpp.IntegrityError):
+        zpp.dequantize(q)
+    q4 = zpp.quantize(torch.ones(8, device="cuda"), zpp.QuantConfig(bit_width=4, block_size=8))
+    q4.codes[0] = 0x88
+    with pytest.raises(zpp.IntegrityError):
+        zpp.dequantize(q4)
+    a = zpp.quantize(torch.ones(8, device="cuda"), zpp.QuantConfig(bit_width=8, block_size=8))
+    b = zpp.quantize(torch.ones(16, device="cuda"), zpp.QuantConfig(bit_width=8, block_size=8))
+    with pytest.raises(zpp.ValidationError):
+        zpp.fused_dequant_reduce_quant([a, b], zpp.QuantConfig(bit_width=8, block_size=8))
+    with pytest.raises(zpp.ValidationError):
+        zpp.fused_dequant_reduce_quant([], zpp.QuantConfig(bit_width=8, block_size=8))
+
+
+def test_fused_golden():
+    zpp = _zpp()
+    z, meta = gu.load("fused")
+    for m in meta:
+        i = m["idx"]
+        icfg = zpp.QuantConfig(bit_width=m["in_bits"], block_size=m["in_block"])
+        ocfg = zpp.QuantConfig(bit_width=m["out_bits"], block_size=m["out_block"])
+        qs = [zpp.quantize(torch.from_numpy(z[f"{i}_in{j}_values"]).cuda(), icfg) for j in range(m["k"])]
+        for j, q in enumerate(qs):
+            assert np.array_equal(q.codes.cpu().numpy(), z[f"{i}_in{j}_codes"])
+        f = zpp.fused_dequant_reduce_quant(qs, ocfg)
+        assert np.array_equal(f.codes.cpu().numpy(), z[f"{i}_codes"]), m
+        assert np.array_equal(f.scales.cpu().numpy(), z[f"{i}_scales"]), m
+        # fused == unfused composition on the device too
+        acc = zpp.dequant_reduce(qs)
+        u = zpp.quantize(acc, ocfg)
+        assert torch.equal(u.codes, f.codes) and torch.equal(u.scales, f.scales)
+
+
+def test_fused_fp32_inputs_all_register_blocks():
+    """K2 register path for every supported output block, fp32-sourced inputs."""
+    zpp = _zpp()
+    g = torch.Generator(device="cpu").manual_seed(5)
+    for ob in (64, 128, 256, 512, 1024, 2048, 24):
+        for ib in (8, 64, 512):
+            for ibits, obits in ((4, 4), (8, 4), (4, 8), (8, 8)):
+                n = 4 * 1024 + 512
+                vals = [torch.randn(n, generator=g) * float(k + 1) for k in range(3)]
+                icfg = zpp.QuantConfig(bit_width=ibits, block_size=ib)
+                ocfg = zpp.QuantConfig(bit_width=obits, block_size=ob)
+                qs = [zpp.quantize(v.float().cuda(), icfg) for v in vals]
+                f = zpp.fused_dequant_reduce_quant(qs, ocfg)
+                ins = []
+                for v in vals:
+                    c, s, _ = O.quantize(v.double().numpy(), ibits, ib)
+                    ins.append((c, s, n, ibits, ib))
+                c, s, _ = O.fused_dequant_reduce_quant(ins, obits, ob)
+                assert np.array_equal(f.codes.cpu().numpy(), c), (ob, ib, ibits, obits)
+                assert np.array_equal(f.scales.cpu().numpy(), s), (ob, ib, ibits, obits)
+
+
+@pytest.mark.parametrize("dtype", ["fp16", "bf16", "fp32"])
+@pytest.mark.parametrize("bits,block", [(8, 2048), (4, 512), (8, 64), (4, 128), (8, 256), (4, 1024), (8, 40),
+                                        (4, 8), (8, 4096)])
+def test_register_and_generic_paths_vs_oracle(dtype, bits, block):
+    """Random heavy-tailed inputs with ragged tails through every dispatch path."""
+    zpp = _zpp()
+    rng = np.random.default_rng(bits * 7919 + block)
+    n = 37 * block + 13
+    v = np.clip(rng.normal(size=n) * np.exp(rng.normal(size=n) * 2), -60000, 60000)
+    if dtype == "fp16":
+        arr = v.astype(np.float16)
+    elif dtype == "bf16":
+        arr = (v.astype(np.float32).view(np.uint32) >> 16).astype(np.uint16)  # truncation is fine for inputs
+    else:
+        arr = v.astype(np.float32)
+    x = gu.to_torch(arr, dtype)
+    q = zpp.quantize(x, zpp.QuantConfig(bit_width=bits, block_size=block))
+    c, s, _ = O.quantize(gu.as_f64(arr, dtype), bits, block)
+    assert np.array_equal(q.codes.cpu().numpy(), c)
+    assert np.array_equal(q.scales.cpu().numpy(), s)
+    ref = O.dequantize(c, s, n, bits, block)
+    for dt, name in [(torch.float16, "fp16"), (torch.float32, "fp32")]:
+        got = zpp.dequantize(q, dt).values.to(torch.float64).cpu().numpy()
+        assert np.array_equal(got, gu.round_to(ref, name))
+
+
+def test_near_tie_adversarial_fp32():
+    """Values engineered to land within a few ulps of k + 0.5 after scaling:
+    the fp32 fast path must hand all of them to the exact f64 path."""
+    zpp = _zpp()
+    rng = np.random.default_rng(77)
+    blocks = []
+    for _ in range(512):
+        m = np.float32(np.exp(rng.normal() * 10))
+        k = rng.integers(-127, 127, size=2047) + 0.5
+        t = (k * np.float64(m) / 127.0).astype(np.float32)
+        t = np.nextafter(t, np.where(rng.random(2047) < 0.5, -np.inf, np.inf).astype(np.float32)) \
+            if rng.random() < 0.5 else t
+        blk = np.concatenate([[m], np.clip(t, -m, m)]).astype(np.float32)
+        blocks.append(rng.permutation(blk))
+    arr = np.concatenate(blocks).astype(np.float32)
+    for bits in (8, 4):
+        q = zpp.quantize(torch.from_numpy(arr).cuda(), zpp.QuantConfig(bit_width=bits, block_size=2048))
+        c, s, _ = O.quantize(arr.astype(np.float64), bits, 2048)
+        assert np.array_equal(q.codes.cpu().numpy(), c)
+        assert np.array_equal(q.scales.cpu().numpy(), s)
+
+
+def test_div_by_qmax_exhaustive_fp32():
+    """The FMA-corrected division by qmax equals IEEE f64 division for every
+    positive finite fp32 absmax (2^31 values) -- scales are bit-exact."""
+    zpp = _zpp()
+    lib = zpp._lib.load()
+    step = 1 << 27
+    out = torch.empty(step, dtype=torch.float64, device="cuda")
+    for start in range(0, 0x7F800000, step):
+        cnt = min(step, 0x7F800000 - start)
+        bits = torch.arange(start, start + cnt, dtype=torch.int64, device="cuda").to(torch.int32)
+        m = bits.view(torch.float32)
+        for b, qm in ((8, 127.0), (4, 7.0)):
+            zpp._lib.check(lib.zpp_scales(m.data_ptr(), zpp._lib.F32, cnt, b, out.data_ptr(),
+                                          torch.cuda.current_stream().cuda_stream))
+            want = m.double() / qm
+            assert torch.equal(out[:cnt], want), (start, b)
+
+
+def test_div_by_qmax_random_f64():
+    zpp = _zpp()
+    lib = zpp._lib.load()
+    g = torch.Generator(device="cuda").manual_seed(3)
+    for _ in range(8):
+        bits = torch.randint(0, 0x7FEFFFFFFFFFFFFF, (1 << 26,), generator=g, device="cuda", dtype=torch.int64)
+        m = bits.view(torch.float64)
+        out = torch.empty_like(m)
+        for b, qm in ((8, 127.0), (4, 7.0)):
+            zpp._lib.check(lib.zpp_scales(m.data_ptr(), zpp._lib.F64, m.numel(), b, out.data_ptr(),
+                                          torch.cuda.current_stream().cuda_stream))
+            assert torch.equal(out, m / qm)
+
+
+def test_config1_full_size_roundtrip():
+    """BASELINE config 1: 16M fp32, INT8/2048, bit-exact vs the oracle at full size."""
+    zpp = _zpp()
+    g = torch.Generator(device="cpu").manual_seed(0)
+    x = (torch.randn(1 << 24, generator=g, dtype=torch.float64) *
+         torch.exp(torch.randn(1 << 24, generator=g, dtype=torch.float64))).float()
+    q = zpp.quantize(x.cuda(), zpp.QuantConfig(bit_width=8, block_size=2048))
+    c, s, _ = O.quantize(x.double().numpy(), 8, 2048)
+    assert np.array_equal(q.codes.cpu().numpy(), c)
+    assert np.array_equal(q.scales.cpu().numpy(), s)
+    back = zpp.dequantize(q, torch.float32).values.cpu().numpy()
+    assert np.array_equal(back, O.dequantize(c, s, x.numel(), 8, 2048).astype(np.float32))
+
+
+def test_empty_and_tiny():
+    zpp = _zpp()
+    q = zpp.quantize(torch.zeros(0, device="cuda"), zpp.QuantConfig(bit_width=8))
+    assert q.n_blocks == 0 and q.codes.numel() == 0
+    assert zpp.dequantize(q).values.numel() == 0
+    for n in range(1, 20):
+        x = torch.linspace(-1, 1, n, device="cuda", dtype=torch.float32)
+        q = zpp.quantize(x, zpp.QuantConfig(bit_width=4, block_size=8))
+        c, s, _ = O.quantize(x.double().cpu().numpy(), 4, 8)
+        assert np.array_equal(q.codes.cpu().numpy(), c)
+
+
+def test_misaligned_input_uses_generic_path():
+    zpp = _zpp()
+    base = torch.randn(4096 + 3, device="cuda", dtype=torch.float16)
+    x = base[3:]  # 6-byte offset: not 16-byte aligned
+    q = zpp.quantize(x, zpp.QuantConfig(bit_width=8, block_size=2048))
+    c, s, _ = O.quantize(x.double().cpu().numpy(), 8, 2048)
+    assert np.array_equal(q.codes.cpu().numpy(), c)
+    assert np.array_equal(q.scales.cpu().numpy(), s)
+
+
+def test_slice_blocks_matches_direct():
+    zpp = _zpp()
+    vals = torch.randn(64, dtype=torch.float64, device="cuda")
+    q = zpp.quantize(vals, zpp.QuantConfig(bit_width=4, block_size=16))
+    part = q.slice_blocks(16, 32)
+    direct = zpp.quantize(vals[16:48], zpp.QuantConfig(bit_width=4, block_size=16))
+    assert torch.equal(part.codes, direct.codes) and torch.equal(part.scales, direct.scales)
+    with pytest.raises(zpp.ValidationError):
+        q.slice_blocks(8, 16)
+
+
+def test_error_bound_half_scale():
+    zpp = _zpp()
+    for bits in (4, 8):
+        x = torch.randn(20000, dtype=torch.float64, device="cuda") * 10
+        st = zpp.quant_error_stats(x, zpp.QuantConfig(bit_width=bits, block_size=512))
+        assert st.per_block_bound_violations == 0 and st.max_abs_error > 0
