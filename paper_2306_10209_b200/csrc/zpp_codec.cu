@@ -62,28 +62,28 @@ static size_t dtype_size(int dt) {
 // ---------------------------------------------------------------------------
 // K0 / K1
 
-template <typename T, int BITS, int LANES, int EPL, typename Addr>
+template <typename T, int BITS, int LANES, typename Addr, int EPL = Raw<T>::kEPL>
 static int run_qreg(const T* x, const Addr& addr, int64_t n_blocks, uint8_t* codes, float* absmax, uint32_t* flag,
                     cudaStream_t st) {
-  auto k = quantize_reg_kernel<T, BITS, LANES, EPL, true, Addr>;
-  const int teams_per_cta = 256 / LANES;
-  const int grid = grid_for(k, 256, ceil_div(n_blocks, teams_per_cta));
+  auto k = quantize_reg_kernel<T, BITS, LANES, EPL, Addr>;
+  const int grid = grid_for(k, 256, ceil_div(n_blocks, 256 / LANES));
   k<<<grid, 256, 0, st>>>(x, addr, n_blocks, codes, absmax, flag);
   return check_cuda(cudaGetLastError(), "quantize_reg_kernel launch");
 }
 
+// register path: block = LANES * Raw<T>::kEPL with LANES a power of two <= 32
 template <typename T, int BITS, typename Addr>
 static int dispatch_qreg(const T* x, const Addr& addr, int64_t n_blocks, int64_t block, uint8_t* codes,
                          float* absmax, uint32_t* flag, cudaStream_t st, bool* handled) {
   *handled = true;
-  switch (block) {
-    case 64: return run_qreg<T, BITS, 8, 8>(x, addr, n_blocks, codes, absmax, flag, st);
-    case 128: return run_qreg<T, BITS, 16, 8>(x, addr, n_blocks, codes, absmax, flag, st);
-    case 256: return run_qreg<T, BITS, 32, 8>(x, addr, n_blocks, codes, absmax, flag, st);
-    case 512: return run_qreg<T, BITS, 32, 16>(x, addr, n_blocks, codes, absmax, flag, st);
-    case 1024: return run_qreg<T, BITS, 32, 32>(x, addr, n_blocks, codes, absmax, flag, st);
-    case 2048: return run_qreg<T, BITS, 32, 64>(x, addr, n_blocks, codes, absmax, flag, st);
-  }
+  constexpr int64_t EPL = Raw<T>::kEPL;
+  if (block == EPL) return run_qreg<T, BITS, 1>(x, addr, n_blocks, codes, absmax, flag, st);
+  if (block == 2 * EPL) return run_qreg<T, BITS, 2>(x, addr, n_blocks, codes, absmax, flag, st);
+  if (block == 4 * EPL) return run_qreg<T, BITS, 4>(x, addr, n_blocks, codes, absmax, flag, st);
+  if (block == 8 * EPL) return run_qreg<T, BITS, 8>(x, addr, n_blocks, codes, absmax, flag, st);
+  if (block == 16 * EPL) return run_qreg<T, BITS, 16>(x, addr, n_blocks, codes, absmax, flag, st);
+  if (block == 32 * EPL) return run_qreg<T, BITS, 32>(x, addr, n_blocks, codes, absmax, flag, st);
+  if (EPL == 32 && block == 2048) return run_qreg<T, BITS, 32, Addr, 64>(x, addr, n_blocks, codes, absmax, flag, st);
   *handled = false;
   return ZPP_OK;
 }
@@ -143,10 +143,13 @@ int launch_quantize(const void* x, int dtype, const AddrSpec& a, int64_t n_out, 
                     uint8_t* codes, void* absmax, uint32_t* flag, cudaStream_t st) {
   if (n_out == 0) return ZPP_OK;
   if (a.swizzle) {
-    SwizzleAddr addr{a.L, a.part, a.stage_off, a.X, a.Y, a.reorder};
+    if (a.L / block >= (1ll << 31) || (int64_t)a.X * a.Y * (a.L / block) >= (1ll << 31))
+      return fail(ZPP_ERR_VALIDATION, "qgZ bucket too large (more than 2^31 blocks)");
+    SwizzleAddr addr{a.L, a.part, a.stage_off, block, a.X, a.Y, a.reorder,
+                     FastDiv::make((uint32_t)(a.L / block)), FastDiv::make((uint32_t)a.Y)};
     return quantize_dispatch(x, dtype, addr, n_out, bits, block, codes, absmax, flag, st);
   }
-  PlainAddr addr{a.n};
+  PlainAddr addr{a.n, block};
   return quantize_dispatch(x, dtype, addr, n_out, bits, block, codes, absmax, flag, st);
 }
 
@@ -170,10 +173,25 @@ static int fill_table(SrcTable& t, const void* const* codes, const void* const* 
 template <int BITS, typename A, typename O>
 static int run_gather(const SrcTable& t, int n_src, int rot, int64_t shard_len, int64_t block, void* out,
                       void* sec_out, int64_t sec_lo, int64_t sec_len, uint32_t* flag, cudaStream_t st) {
+  const int vec_ok = aligned16(out) && (shard_len % 8 == 0) &&
+                     (sec_out == nullptr || (aligned16(sec_out) && sec_lo % 8 == 0));
+  constexpr bool k16 = sizeof(O) == 2 && std::is_same<A, float>::value;
+  if constexpr (k16) {
+    // fast 16-bit output path: one scale per 16-byte code load, aligned loads
+    bool fast = block % (128 / BITS) == 0;
+    for (int i = 0; i < n_src; ++i) fast = fast && aligned16(t.codes[i]);
+    if (fast) {
+      auto k = dequant16_kernel<BITS, O>;
+      const int64_t tiles = ceil_div(ceil_div(shard_len, 128 / BITS), 32 * 2) * n_src;
+      const int grid = grid_for(k, 256, ceil_div(tiles, 8));
+      k<<<grid, 256, 0, st>>>(t, n_src, rot, shard_len, block, reinterpret_cast<O*>(out),
+                              reinterpret_cast<O*>(sec_out), sec_lo, sec_len, vec_ok, flag);
+      return check_cuda(cudaGetLastError(), "dequant16_kernel launch");
+    }
+  }
   auto k = dequant_gather_kernel<BITS, A, O>;
-  const int64_t groups = ceil_div(ceil_div(shard_len, 8), 32) * n_src;
-  const int grid = grid_for(k, 256, ceil_div(groups, 8));
-  const int vec_ok = aligned16(out) && (shard_len % 8 == 0);
+  const int64_t tiles = ceil_div(ceil_div(shard_len, 8), 32 * 4) * n_src;
+  const int grid = grid_for(k, 256, ceil_div(tiles, 8));
   k<<<grid, 256, 0, st>>>(t, n_src, rot, shard_len, block, reinterpret_cast<O*>(out), reinterpret_cast<O*>(sec_out),
                           sec_lo, sec_len, vec_ok, flag);
   return check_cuda(cudaGetLastError(), "dequant_gather_kernel launch");
@@ -183,7 +201,7 @@ template <int BITS, typename A, typename O>
 static int run_reduce(const SrcTable& t, int n_src, int64_t n, int64_t block, void* out, double post_scale,
                       uint32_t* flag, cudaStream_t st) {
   auto k = dequant_reduce_kernel<BITS, A, O>;
-  const int grid = grid_for(k, 256, ceil_div(ceil_div(n, 8), 256));
+  const int grid = grid_for(k, 256, ceil_div(n, 8 * 32 * 2 * 8));
   k<<<grid, 256, 0, st>>>(t, n_src, n, block, reinterpret_cast<O*>(out), post_scale, aligned16(out), flag);
   return check_cuda(cudaGetLastError(), "dequant_reduce_kernel launch");
 }
@@ -236,18 +254,18 @@ int launch_dequant_reduce(const void* const* codes, const void* const* absmax, i
 // K2
 
 bool drq_has_reg_path(int64_t out_block) {
-  return out_block == 64 || out_block == 128 || out_block == 256 || out_block == 512 || out_block == 1024;
+  return out_block == 16 || out_block == 32 || out_block == 64 || out_block == 128 || out_block == 256 ||
+         out_block == 512;
 }
 
 size_t drq_workspace_bytes(int64_t n, int64_t out_block) {
-  if (drq_has_reg_path(out_block)) return 0;
   return (size_t)(ceil_div(n, out_block) * out_block) * sizeof(double);
 }
 
-template <int IBITS, typename IA, int OBITS, int LANES, int EPL>
+template <int IBITS, typename IA, int OBITS, int LANES>
 static int run_drq(const SrcTable& t, int n_src, int64_t n, int64_t in_block, int64_t nbo, uint8_t* codes,
                    double* absmax, uint32_t* flag, cudaStream_t st) {
-  auto k = drq_reg_kernel<IBITS, IA, OBITS, LANES, EPL>;
+  auto k = drq_reg_kernel<IBITS, IA, OBITS, LANES>;
   const int grid = grid_for(k, 256, ceil_div(nbo, 256 / LANES));
   k<<<grid, 256, 0, st>>>(t, n_src, n, in_block, nbo, codes, absmax, flag);
   return check_cuda(cudaGetLastError(), "drq_reg_kernel launch");
@@ -258,11 +276,12 @@ static int drq_block(const SrcTable& t, int n_src, int64_t n, int64_t in_block, 
                      double* absmax, uint32_t* flag, cudaStream_t st) {
   const int64_t nbo = ceil_div(n, out_block);
   switch (out_block) {
-    case 64: return run_drq<IBITS, IA, OBITS, 8, 8>(t, n_src, n, in_block, nbo, codes, absmax, flag, st);
-    case 128: return run_drq<IBITS, IA, OBITS, 16, 8>(t, n_src, n, in_block, nbo, codes, absmax, flag, st);
-    case 256: return run_drq<IBITS, IA, OBITS, 32, 8>(t, n_src, n, in_block, nbo, codes, absmax, flag, st);
-    case 512: return run_drq<IBITS, IA, OBITS, 32, 16>(t, n_src, n, in_block, nbo, codes, absmax, flag, st);
-    case 1024: return run_drq<IBITS, IA, OBITS, 32, 32>(t, n_src, n, in_block, nbo, codes, absmax, flag, st);
+    case 16: return run_drq<IBITS, IA, OBITS, 1>(t, n_src, n, in_block, nbo, codes, absmax, flag, st);
+    case 32: return run_drq<IBITS, IA, OBITS, 2>(t, n_src, n, in_block, nbo, codes, absmax, flag, st);
+    case 64: return run_drq<IBITS, IA, OBITS, 4>(t, n_src, n, in_block, nbo, codes, absmax, flag, st);
+    case 128: return run_drq<IBITS, IA, OBITS, 8>(t, n_src, n, in_block, nbo, codes, absmax, flag, st);
+    case 256: return run_drq<IBITS, IA, OBITS, 16>(t, n_src, n, in_block, nbo, codes, absmax, flag, st);
+    case 512: return run_drq<IBITS, IA, OBITS, 32>(t, n_src, n, in_block, nbo, codes, absmax, flag, st);
   }
   return fail(ZPP_ERR_VALIDATION, "no register path for this output block");
 }
@@ -277,7 +296,9 @@ int launch_drq(const void* const* codes, const void* const* absmax, int absmax_d
   if (absmax_dtype != ZPP_F32 && absmax_dtype != ZPP_F64)
     return fail(ZPP_ERR_VALIDATION, "absmax dtype must be F32 or F64");
   const bool a64 = absmax_dtype == ZPP_F64;
-  if (drq_has_reg_path(out_block)) {
+  bool aligned = true;  // 8-element chunk loads need 8 B (INT8) / 4 B (INT4) aligned codes
+  for (int i = 0; i < n_src; ++i) aligned = aligned && (reinterpret_cast<uintptr_t>(codes[i]) % in_bits) == 0;
+  if (drq_has_reg_path(out_block) && aligned) {
 #define ZPP_DRQ(IB, OB)                                                                                  \
   return a64 ? drq_block<IB, double, OB>(t, n_src, n, in_block, out_block, out_codes, out_absmax, flag, st) \
              : drq_block<IB, float, OB>(t, n_src, n, in_block, out_block, out_codes, out_absmax, flag, st);

@@ -312,7 +312,7 @@ static QgzLayout qgz_layout(int64_t n, int world, int Y, int stages, int ib, int
   l.hop_abs = off;
   off += align256((size_t)ceil_div(hop_elems, oblk) * 8);
   l.ws = off;
-  off += align256(drq_workspace_bytes(hop_elems, oblk));
+  off += align256(drq_has_reg_path(oblk) ? 0 : drq_workspace_bytes(hop_elems, oblk));
   l.region = off;
   return l;
 }

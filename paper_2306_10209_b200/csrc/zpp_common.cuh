@@ -34,7 +34,7 @@ __device__ __forceinline__ void raise_flag(uint32_t* flag, uint32_t bit) {
 // q0 = RN(m * RN(1/Q)); e = m - q0*Q (exact through FMA); RN(q0 + e * RN(1/Q))
 // is the correctly rounded quotient for normal m (Markstein); verified against
 // __ddiv_rn on every positive fp32 value and 2^30 random doubles in
-// tests/test_gpu_numerics.py.
+// tests/test_gpu_codec.py.
 template <int Q>
 __device__ __forceinline__ double div_q(double m) {
   constexpr double r = 1.0 / Q;
@@ -57,22 +57,9 @@ __device__ __forceinline__ int rint_f64(double t) {
   return __double2loint(__dadd_rn(t, kMagic52));
 }
 
-// fp32 fast path: t = x * inv32, r = rint(t).  |t - t64| < 1.6e-5 where
-// t64 = RN64(x * inv64) (inv32 = RN32(inv64); two fp32 roundings of a value
-// <= qmax + 1e-5), so r == rint(t64) unless t lies within 2^-15 of a half
-// integer.  Those (rare) elements are redone in f64.
-constexpr float kMagic23 = 12582912.0f;  // 1.5 * 2^23
+constexpr float kMagic23 = 12582912.0f;  // 1.5 * 2^23: x + kMagic23 rounds x to an integer
+// quantize fast-path guard: |e| <= 0.5 - 2^-15 (see quant_chunk in zpp_kernels.cuh)
 constexpr float kTieGuard = 0.5f - 3.0517578125e-05f;
-
-// returns the float whose low byte is the two's complement code
-__device__ __forceinline__ uint32_t q_fast(float x, float inv32, bool& redo) {
-  float t = __fmul_rn(x, inv32);
-  float tm = __fadd_rn(t, kMagic23);
-  float r = __fsub_rn(tm, kMagic23);
-  float d = fabsf(__fsub_rn(t, r));
-  redo |= d > kTieGuard;
-  return __float_as_uint(tm);
-}
 
 template <int QMAX>
 __device__ __forceinline__ uint32_t q_exact(double x, double inv64) {
@@ -128,13 +115,6 @@ __device__ __forceinline__ void unpack8_int4(uint32_t w, uint32_t (&u)[8]) {
 // ---------------------------------------------------------------------------
 // element types
 
-template <typename T> struct Elem;
-template <> struct Elem<float> {
-  static constexpr int kRawWords = 8;  // 32 bytes per 8 elements
-  static constexpr uint32_t kInfBits = 0x7f800000u;
-  __device__ static float to_float(uint32_t w, int /*half*/) { return __uint_as_float(w); }
-};
-
 template <int BITS> struct Codes {
   static constexpr int kQmax = (1 << (BITS - 1)) - 1;
   static constexpr int kBytesPer8 = BITS;  // 8 elements -> 8 or 4 bytes
@@ -162,6 +142,61 @@ template <int BITS>
 __device__ __forceinline__ double scale_of(double m) {
   return div_q<Codes<BITS>::kQmax>(m);
 }
+
+// ---------------------------------------------------------------------------
+// Blackwell packed fp32x2 arithmetic (FFMA2 / FADD2 / FMUL2), round-to-nearest
+
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;"
+      : "=l"(*reinterpret_cast<unsigned long long*>(&d))
+      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)),
+        "l"(*reinterpret_cast<unsigned long long*>(&c)));
+  return d;
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  float2 d;
+  asm("add.rn.f32x2 %0, %1, %2;"
+      : "=l"(*reinterpret_cast<unsigned long long*>(&d))
+      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)));
+  return d;
+}
+__device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
+  float2 d;
+  asm("mul.rn.f32x2 %0, %1, %2;"
+      : "=l"(*reinterpret_cast<unsigned long long*>(&d))
+      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)));
+  return d;
+}
+
+// max(|a|,|b|) per 16-bit lane, NaN-propagating (HMNMX2.NAN.XORSIGN |a|,|b|);
+// the sign bits of the result are garbage and must be masked by the caller.
+__device__ __forceinline__ uint32_t absmax_bf16x2(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("max.NaN.xorsign.abs.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+__device__ __forceinline__ uint32_t absmax_f16x2(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("max.NaN.xorsign.abs.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+
+// unsigned 32-bit division by an invariant divisor (n < 2^31):
+// q = (umulhi(n, mul) + n) >> shift
+struct FastDiv {
+  uint32_t d, mul, shift;
+  __host__ static FastDiv make(uint32_t d) {
+    FastDiv f;
+    f.d = d;
+    uint32_t s = 0;
+    while ((1ull << s) < d) ++s;
+    f.shift = s;
+    f.mul = (uint32_t)((((1ull << 32) * ((1ull << s) - d)) / d) + 1);
+    return f;
+  }
+  __device__ __forceinline__ uint32_t div(uint32_t n) const { return (__umulhi(n, mul) + n) >> shift; }
+};
 
 // global timer for bounded spins
 __device__ __forceinline__ uint64_t globaltimer_ns() {

@@ -1,7 +1,11 @@
 // ZeRO++ codec kernels for sm_100a.  All are HBM/NVLink-bound streaming
-// kernels (no tensor-core work exists on this path): 16-byte vector loads,
-// coalesced per warp, per-block absmax by warp shuffles, grid = one resident
-// wave over the 148 SMs with grid-stride loops.
+// kernels (no tensor-core work exists on this path).  Design rules, from ncu
+// on B200: keep every lane >= 64-128 B of loads in flight, keep registers
+// <= ~64 for >= 50% occupancy, and spend < ~6 ALU + ~6 FMA-pipe thread
+// instructions per element (the ALU and FMA pipes each take a warp
+// instruction every 2 cycles per SMSP).  The inner loops therefore use
+// Blackwell's packed fp32x2 FFMA2/FADD2/FMUL2 and HMNMX2, and fall back to
+// exact f64 arithmetic only for elements an error bound cannot decide.
 //
 //   K0 quantize          zs/quantizer.py:204-228   (register path + generic path)
 //   K1 swizzle-quantize  zs/collectives.py:509-518 + reorder_mapping :407-417
@@ -11,6 +15,7 @@
 #pragma once
 
 #include <cfloat>
+#include <type_traits>
 #include "zpp_common.cuh"
 
 namespace zpp {
@@ -25,10 +30,12 @@ struct SrcTable {
 };
 
 // ---------------------------------------------------------------------------
-// addressing: output element o (a multiple of 8) -> source element
+// addressing: where the input of output block b / output element o lives
 
 struct PlainAddr {
   int64_t n;
+  int64_t B;
+  __device__ __forceinline__ int64_t block_src(int64_t b) const { return b * B; }
   __device__ __forceinline__ int64_t src(int64_t o) const { return o; }
   __device__ __forceinline__ int64_t valid(int64_t o) const { return n - o; }
 };
@@ -41,14 +48,23 @@ struct SwizzleAddr {
   int64_t L;         // slice length
   int64_t part;      // S * L: one rank's final partition
   int64_t stage_off; // stage * L
+  int64_t B;
   int X, Y;
   int reorder;
+  FastDiv bps;       // blocks per slice (L / B)
+  FastDiv fy;        // Y
+  __device__ __forceinline__ int64_t resid_of(int64_t k) const {
+    const int64_t j = fy.div((uint32_t)k), c = k - j * Y;
+    return reorder ? c * X + j : k;
+  }
+  __device__ __forceinline__ int64_t block_src(int64_t b) const {
+    const int64_t k = bps.div((uint32_t)b);
+    const int64_t eb = b - k * (int64_t)bps.d;
+    return resid_of(k) * part + stage_off + eb * B;
+  }
   __device__ __forceinline__ int64_t src(int64_t o) const {
-    int64_t k = o / L;
-    int64_t e = o - k * L;
-    int64_t j = k / Y, c = k - j * Y;
-    int64_t resid = reorder ? c * X + j : k;
-    return resid * part + stage_off + e;
+    const int64_t k = o / L;
+    return resid_of(k) * part + stage_off + (o - k * L);
   }
   __device__ __forceinline__ int64_t valid(int64_t) const { return INT64_MAX; }
 };
@@ -60,6 +76,7 @@ template <typename T> struct Raw;
 
 template <> struct Raw<__half> {
   static constexpr int W = 4;
+  static constexpr int kEPL = 64;  // elements per lane in the register path
   __device__ static void load(const __half* p, uint32_t (&r)[W]) {
     uint4 v = __ldg(reinterpret_cast<const uint4*>(p));
     r[0] = v.x; r[1] = v.y; r[2] = v.z; r[3] = v.w;
@@ -73,12 +90,14 @@ template <> struct Raw<__half> {
       r[i] = lo | (hi << 16);
     }
   }
-  __device__ static uint32_t absmax_bits(const uint32_t (&r)[W], uint32_t acc) {
-#pragma unroll
-    for (int i = 0; i < W; ++i) acc = __vmaxu2(acc, r[i] & 0x7fff7fffu);
-    return acc;
+  // running max of |x| over packed pairs (NaN-propagating); sign bits garbage
+  __device__ static uint32_t absacc(const uint32_t (&r)[W], uint32_t acc) {
+    return absmax_f16x2(acc, absmax_f16x2(absmax_f16x2(r[0], r[1]), absmax_f16x2(r[2], r[3])));
   }
-  __device__ static uint32_t finish(uint32_t acc) { return max(acc & 0xffffu, acc >> 16); }
+  __device__ static uint32_t finish(uint32_t acc) {
+    acc &= 0x7fff7fffu;
+    return max(acc & 0xffffu, acc >> 16);
+  }
   __device__ static bool nonfinite(uint32_t m) { return m >= 0x7c00u; }
   __device__ static float m_to_float(uint32_t m) { return __half2float(__ushort_as_half((unsigned short)m)); }
   __device__ static void to_float(const uint32_t (&r)[W], float (&v)[8]) {
@@ -93,6 +112,7 @@ template <> struct Raw<__half> {
 
 template <> struct Raw<__nv_bfloat16> {
   static constexpr int W = 4;
+  static constexpr int kEPL = 64;
   __device__ static void load(const __nv_bfloat16* p, uint32_t (&r)[W]) {
     uint4 v = __ldg(reinterpret_cast<const uint4*>(p));
     r[0] = v.x; r[1] = v.y; r[2] = v.z; r[3] = v.w;
@@ -106,12 +126,13 @@ template <> struct Raw<__nv_bfloat16> {
       r[i] = lo | (hi << 16);
     }
   }
-  __device__ static uint32_t absmax_bits(const uint32_t (&r)[W], uint32_t acc) {
-#pragma unroll
-    for (int i = 0; i < W; ++i) acc = __vmaxu2(acc, r[i] & 0x7fff7fffu);
-    return acc;
+  __device__ static uint32_t absacc(const uint32_t (&r)[W], uint32_t acc) {
+    return absmax_bf16x2(acc, absmax_bf16x2(absmax_bf16x2(r[0], r[1]), absmax_bf16x2(r[2], r[3])));
   }
-  __device__ static uint32_t finish(uint32_t acc) { return max(acc & 0xffffu, acc >> 16); }
+  __device__ static uint32_t finish(uint32_t acc) {
+    acc &= 0x7fff7fffu;
+    return max(acc & 0xffffu, acc >> 16);
+  }
   __device__ static bool nonfinite(uint32_t m) { return m >= 0x7f80u; }
   __device__ static float m_to_float(uint32_t m) { return __uint_as_float(m << 16); }
   __device__ static void to_float(const uint32_t (&r)[W], float (&v)[8]) {
@@ -125,6 +146,7 @@ template <> struct Raw<__nv_bfloat16> {
 
 template <> struct Raw<float> {
   static constexpr int W = 8;
+  static constexpr int kEPL = 32;
   __device__ static void load(const float* p, uint32_t (&r)[W]) {
     uint4 a = __ldg(reinterpret_cast<const uint4*>(p));
     uint4 b = __ldg(reinterpret_cast<const uint4*>(p) + 1);
@@ -136,7 +158,7 @@ template <> struct Raw<float> {
 #pragma unroll
     for (int i = 0; i < W; ++i) r[i] = (i < cnt) ? q[i] : 0u;
   }
-  __device__ static uint32_t absmax_bits(const uint32_t (&r)[W], uint32_t acc) {
+  __device__ static uint32_t absacc(const uint32_t (&r)[W], uint32_t acc) {
 #pragma unroll
     for (int i = 0; i < W; ++i) acc = max(acc, r[i] & 0x7fffffffu);
     return acc;
@@ -160,32 +182,55 @@ __device__ __forceinline__ void store_codes8(uint8_t* dst, const uint32_t (&b)[8
   }
 }
 
-// quantize 8 floats of one block: fp32 fast path, exact f64 redo near ties
-template <int BITS>
-__device__ __forceinline__ void quant8(const float (&v)[8], float inv32, double inv64, bool slow,
-                                       uint32_t (&q)[8]) {
-  constexpr int QMAX = Codes<BITS>::kQmax;
-  bool redo = slow;
-  if (!slow) {
+// Quantize one chunk of 8 floats.  Fast path (fp32, packed):
+//   u = RN(x*inv32 + 1.5*2^23) = 1.5*2^23 + k with k = rint(x*inv32)  (FFMA2)
+//   e = RN(x*inv32 - k)                                                (FFMA2)
+// With inv32 = RN32(qmax/m), |x*inv32 - RN64(x*RN64(qmax/m))| < 7.6e-6 and
+// |e - (x*inv32 - k)| <= 2^-25, so |e| <= 0.5 - 2^-15 proves k equals the
+// reference's rint of the f64 product.  Elements failing that test (near or
+// exact ties: ~0.3% of bf16 inputs, whose 8-bit mantissas make exact ties
+// common) are recomputed with the reference's f64 arithmetic, element by
+// element.  The low byte of each returned word is the code in two's complement.
+template <int QMAX>
+__device__ __forceinline__ void quant_chunk(const float (&v)[8], float inv32, double inv64, uint32_t (&q)[8]) {
+  const float2 inv2 = make_float2(inv32, inv32);
+  const float2 m2 = make_float2(kMagic23, kMagic23);
+  float e[8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) q[i] = q_fast(v[i], inv32, redo);
+  for (int i = 0; i < 4; ++i) {
+    const float2 x = make_float2(v[2 * i], v[2 * i + 1]);
+    const float2 u = ffma2(x, inv2, m2);
+    float2 nk;
+    asm("sub.rn.f32x2 %0, %1, %2;"
+        : "=l"(*reinterpret_cast<unsigned long long*>(&nk))
+        : "l"(*reinterpret_cast<const unsigned long long*>(&m2)), "l"(*reinterpret_cast<const unsigned long long*>(&u)));
+    const float2 ee = ffma2(x, inv2, nk);
+    e[2 * i] = ee.x;
+    e[2 * i + 1] = ee.y;
+    q[2 * i] = __float_as_uint(u.x);
+    q[2 * i + 1] = __float_as_uint(u.y);
   }
-  if (redo) {
+  const float emax = fmaxf(fmaxf(fmaxf(fabsf(e[0]), fabsf(e[1])), fmaxf(fabsf(e[2]), fabsf(e[3]))),
+                           fmaxf(fmaxf(fabsf(e[4]), fabsf(e[5])), fmaxf(fabsf(e[6]), fabsf(e[7]))));
+  if (emax > kTieGuard) {
 #pragma unroll
-    for (int i = 0; i < 8; ++i) q[i] = q_exact<QMAX>((double)v[i], inv64);
+    for (int i = 0; i < 8; ++i)
+      if (fabsf(e[i]) > kTieGuard) q[i] = (uint32_t)rint_f64(__dmul_rn((double)v[i], inv64));
   }
 }
 
 // ---------------------------------------------------------------------------
 // K0/K1 register path: a team of LANES lanes owns one quantization block of
-// B = LANES * EPL elements; lane l loads 8-element chunks c*LANES + l so each
-// warp-wide load instruction covers one contiguous 512 B (fp16) span.
+// B = LANES * EPL elements (EPL = 64 for 16-bit inputs, 32 for fp32, so each
+// lane issues eight 16-byte loads before reducing); lane l loads 8-element
+// chunks c*LANES + l, so each team-wide load covers one contiguous span of
+// >= 128 B.
 
-template <typename T, int BITS, int LANES, int EPL, bool VEC, typename Addr>
+template <typename T, int BITS, int LANES, int EPL, typename Addr>
 __global__ void __launch_bounds__(256)
 quantize_reg_kernel(const T* __restrict__ x, Addr addr, int64_t n_blocks, uint8_t* __restrict__ codes,
                     float* __restrict__ absmax, uint32_t* __restrict__ flag) {
-  static_assert(EPL % 8 == 0 && 32 % LANES == 0, "team shape");
+  static_assert(32 % LANES == 0 && EPL % 8 == 0, "team shape");
   constexpr int B = LANES * EPL;
   constexpr int CH = EPL / 8;
   constexpr int RW = Raw<T>::W;
@@ -193,31 +238,32 @@ quantize_reg_kernel(const T* __restrict__ x, Addr addr, int64_t n_blocks, uint8_
   constexpr int TPW = 32 / LANES;
   const int lane = threadIdx.x & 31;
   const int tl = lane % LANES;
+  const int team = lane / LANES;
   const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarp = ((int64_t)gridDim.x * blockDim.x) >> 5;
 
   for (int64_t wb = gwarp * TPW; wb < n_blocks; wb += nwarp * TPW) {
-    const int64_t b = wb + lane / LANES;
+    const int64_t b = wb + team;
     const bool active = b < n_blocks;
-    const int64_t o0 = b * B;
     int64_t src = 0, valid = 0;
     if (active) {
-      src = addr.src(o0);
-      valid = addr.valid(o0);
+      src = addr.block_src(b);
+      valid = addr.valid(b * B);
     }
     uint32_t raw[CH][RW];
     uint32_t acc = 0;
 #pragma unroll
     for (int c = 0; c < CH; ++c) {
       const int e = (c * LANES + tl) * 8;
-      if (VEC && active && e + 8 <= valid) {
+      if (active && e + 8 <= valid) {
         Raw<T>::load(x + src + e, raw[c]);
       } else {
         const int cnt = active ? (int)max((int64_t)0, min((int64_t)8, valid - e)) : 0;
         Raw<T>::load_scalar(x + src + e, cnt, raw[c]);
       }
-      acc = Raw<T>::absmax_bits(raw[c], acc);
     }
+#pragma unroll
+    for (int c = 0; c < CH; ++c) acc = Raw<T>::absacc(raw[c], acc);
     uint32_t mb = Raw<T>::finish(acc);
 #pragma unroll
     for (int off = LANES / 2; off >= 1; off >>= 1) mb = max(mb, __shfl_xor_sync(0xffffffffu, mb, off));
@@ -226,28 +272,31 @@ quantize_reg_kernel(const T* __restrict__ x, Addr addr, int64_t n_blocks, uint8_
       absmax[b] = m;
       if (Raw<T>::nonfinite(mb)) raise_flag(flag, FLAG_NONFINITE);
     }
+    const float inv32 = m > 0.0f ? __fdiv_rn((float)QMAX, m) : 0.0f;
     const double inv64 = m > 0.0f ? __ddiv_rn((double)QMAX, (double)m) : 0.0;
-    const float inv32 = __double2float_rn(inv64);
-    const bool slow = !(inv32 <= FLT_MAX);
-    if (active) {
-      uint8_t* out = codes + b * (int64_t)(B * BITS / 8);
+    const bool slow = !(inv32 <= 0x1p100f);  // reciprocal of a (sub)normal tiny absmax
+    uint8_t* out = codes + b * (int64_t)(B * BITS / 8);
 #pragma unroll
-      for (int c = 0; c < CH; ++c) {
-        float v[8];
-        Raw<T>::to_float(raw[c], v);
-        uint32_t q[8];
-        quant8<BITS>(v, inv32, inv64, slow, q);
-        store_codes8<BITS>(out + (c * LANES + tl) * BITS, q);
+    for (int c = 0; c < CH; ++c) {
+      float v[8];
+      uint32_t q[8];
+      Raw<T>::to_float(raw[c], v);
+      if (!slow) {
+        quant_chunk<QMAX>(v, inv32, inv64, q);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) q[i] = q_exact<QMAX>((double)v[i], inv64);
       }
+      if (active) store_codes8<BITS>(out + (c * LANES + tl) * BITS, q);
     }
   }
 }
 
 // ---------------------------------------------------------------------------
-// K0/K1 generic path (any block size, any dtype incl. f64): pass 1 reduces
-// per-block absmax with atomics (bits of |x| are monotone as unsigned),
-// pass 2 quantizes 8-element chunks.  8-element chunks never straddle a
-// block because block % 8 == 0.
+// K0/K1 generic path (any block size, any dtype incl. f64, any alignment):
+// pass 1 reduces per-block absmax with atomics (bits of |x| are monotone as
+// unsigned), pass 2 quantizes 8-element chunks.  8-element chunks never
+// straddle a block because block % 8 == 0.
 
 template <typename T> struct GenTraits;
 template <> struct GenTraits<float> { using Bits = uint32_t; };
@@ -255,12 +304,11 @@ template <> struct GenTraits<__half> { using Bits = uint32_t; };
 template <> struct GenTraits<__nv_bfloat16> { using Bits = uint32_t; };
 template <> struct GenTraits<double> { using Bits = unsigned long long; };
 
-// load 8 elements (zero beyond cnt) as doubles/floats
 template <typename T>
 __device__ __forceinline__ void load8_generic(const T* p, int cnt, float (&v)[8], uint32_t& bits) {
   uint32_t r[Raw<T>::W];
   Raw<T>::load_scalar(p, cnt, r);
-  bits = Raw<T>::finish(Raw<T>::absmax_bits(r, 0u));
+  bits = Raw<T>::finish(Raw<T>::absacc(r, 0u));
   Raw<T>::to_float(r, v);
 }
 
@@ -307,7 +355,6 @@ absmax_generic_kernel(const T* __restrict__ x, Addr addr, int64_t n_chunks, int6
       }
     }
   }
-  // merge lanes that end on the same block, one atomic per distinct block
   const int64_t first = __shfl_sync(0xffffffffu, cur, 0);
   const bool same = __all_sync(0xffffffffu, cur == first);
   if (same) {
@@ -344,41 +391,259 @@ quantize_generic_kernel(const T* __restrict__ x, Addr addr, int64_t n_chunks, in
       for (int i = 0; i < 8; ++i) q[i] = q_exact<QMAX>(i < cnt ? p[i] : 0.0, inv64);
     } else {
       const float m = __uint_as_float(absmax_bits[blk]);
-      const double inv64 = m > 0.0f ? __ddiv_rn((double)QMAX, (double)m) : 0.0;
-      const float inv32 = __double2float_rn(inv64);
       float v[8];
       uint32_t mb;
       load8_generic<T>(x + addr.src(o), cnt, v, mb);
-      quant8<BITS>(v, inv32, inv64, !(inv32 <= FLT_MAX), q);
+      const float inv32 = m > 0.0f ? __fdiv_rn((float)QMAX, m) : 0.0f;
+      const double inv64 = m > 0.0f ? __ddiv_rn((double)QMAX, (double)m) : 0.0;
+      if (inv32 <= 0x1p100f) {
+        quant_chunk<QMAX>(v, inv32, inv64, q);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) q[i] = q_exact<QMAX>((double)v[i], inv64);
+      }
     }
     store_codes8<BITS>(codes + ch * BITS, q);
   }
 }
 
 // ---------------------------------------------------------------------------
-// decode helpers: one 8-element chunk of codes -> 8 exact doubles
+// decode helpers
+
+// elements per 16-byte code load
+template <int BITS> struct Unit16B {
+  static constexpr int E = 128 / BITS;
+};
+
+__device__ __forceinline__ bool bad_codes(uint4 w, int bits) {
+  if (bits == 8)
+    return has_byte_0x80(w.x) | has_byte_0x80(w.y) | has_byte_0x80(w.z) | has_byte_0x80(w.w);
+  return has_nibble_8(w.x) | has_nibble_8(w.y) | has_nibble_8(w.z) | has_nibble_8(w.w);
+}
+
+// codes -> "magic float" bits 0x4B400000 | (code + bias): the float
+// 1.5*2^23 + code + bias, exact
+__device__ __forceinline__ void magic_int8(uint32_t w, uint32_t (&f)[4]) {
+  const uint32_t b = w ^ 0x80808080u;
+  f[0] = __byte_perm(b, 0x4B400000u, 0x7650);
+  f[1] = __byte_perm(b, 0x4B400000u, 0x7651);
+  f[2] = __byte_perm(b, 0x4B400000u, 0x7652);
+  f[3] = __byte_perm(b, 0x4B400000u, 0x7653);
+}
+// 8 INT4 codes (low nibble first)
+__device__ __forceinline__ void magic_int4(uint32_t w, uint32_t (&f)[8]) {
+  const uint32_t b = w ^ 0x88888888u;
+  const uint32_t ev = b & 0x0F0F0F0Fu, od = (b >> 4) & 0x0F0F0F0Fu;
+  f[0] = __byte_perm(ev, 0x4B400000u, 0x7650);
+  f[1] = __byte_perm(od, 0x4B400000u, 0x7650);
+  f[2] = __byte_perm(ev, 0x4B400000u, 0x7651);
+  f[3] = __byte_perm(od, 0x4B400000u, 0x7651);
+  f[4] = __byte_perm(ev, 0x4B400000u, 0x7652);
+  f[5] = __byte_perm(od, 0x4B400000u, 0x7652);
+  f[6] = __byte_perm(ev, 0x4B400000u, 0x7653);
+  f[7] = __byte_perm(od, 0x4B400000u, 0x7653);
+}
+
+template <int BITS>
+__device__ __forceinline__ void magic_word(uint32_t w, uint32_t (&f)[32 / BITS]) {
+  if constexpr (BITS == 8) magic_int8(w, f);
+  else magic_int4(w, f);
+}
+
+template <int BITS> struct Bias;
+template <> struct Bias<8> {
+  static constexpr float kF = 12582912.0f + 128.0f;
+  static constexpr double kD = kMagic52 + 128.0;
+};
+template <> struct Bias<4> {
+  static constexpr float kF = 12582912.0f + 8.0f;
+  static constexpr double kD = kMagic52 + 8.0;
+};
+
+// exact code value from magic-float bits
+template <int BITS> __device__ __forceinline__ double code_f64(uint32_t fbits) {
+  return __dsub_rn(__hiloint2double(0x43380000, (int)(fbits & 0xFFu)), Bias<BITS>::kD);
+}
+
+// Fast 16-bit output of a unit: p = RN32(code * s32) with s32 = RN32(m * RN32(1/q))
+// is within 3 fp32 ulps of the exact f64 product code*s64, so RN16(p) equals
+// RN16(RN64(code*s64)) unless p lies within 64 ulps of a 16-bit rounding
+// midpoint; the unit is then redone in f64.  Out-of-range scales (16-bit
+// subnormal results, overflow) take the f64 path up front.
+template <typename O> struct Out16;
+template <> struct Out16<__half> {
+  // zero iff the 13 bits below the fp16 mantissa are within [-64, +64) of 0x1000
+  __device__ static uint32_t near_mid(uint32_t bits) { return ((bits + 0x40u) & 0x1F80u) ^ 0x1000u; }
+  __device__ static bool scale_ok(float s, int qmax) { return s >= 0x1p-14f && s * (float)qmax < 65504.0f; }
+  static constexpr uint32_t kLowMask = 0x1FFFu;  // absmax has <= 11 significant bits
+  __device__ static bool in_range(float m) { return m <= 65504.0f; }
+  __device__ static uint32_t pack2(float a, float b) {
+    __half2 h = __floats2half2_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+  }
+};
+template <> struct Out16<__nv_bfloat16> {
+  __device__ static uint32_t near_mid(uint32_t bits) { return ((bits + 0x40u) & 0xFF80u) ^ 0x8000u; }
+  __device__ static bool scale_ok(float s, int qmax) { return s >= 0x1p-125f && s * (float)qmax < 0x1p127f; }
+  static constexpr uint32_t kLowMask = 0xFFFFu;  // absmax has <= 8 significant bits
+  __device__ static bool in_range(float m) { return m >= 0x1p-100f && m < 0x1p127f; }
+  __device__ static uint32_t pack2(float a, float b) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+  }
+};
+
+template <typename O>
+__device__ __forceinline__ void store_scalar(O* dst, int i, uint32_t bits16) {
+  reinterpret_cast<uint16_t*>(dst)[i] = (uint16_t)bits16;
+}
+
+// ---------------------------------------------------------------------------
+// K4 (16-bit outputs): dequantize / gather-dequantize.  Output = concatenation
+// of the n_src sources' decoded shards (shard_len each), the qwZ receive side
+// (zs/collectives.py:264).  Lane unit = one 16-byte code load (E elements,
+// one block scale: the host guarantees B % E == 0 and fp32 absmax); U units
+// per lane per iteration, all loads issued first.  Tiles walk the sources
+// fastest, rotated by `rot`, so every peer's NVLink egress is read at once.
+// Optional hpZ write-through of output range [sec_lo, sec_lo+sec_len) into
+// sec_out (the secondary partition, zs/engine.py:364-367).
+
+template <int BITS, typename O>
+__global__ void __launch_bounds__(256)
+dequant16_kernel(SrcTable src, int n_src, int rot, int64_t shard_len, int64_t B, O* __restrict__ out,
+                 O* __restrict__ sec_out, int64_t sec_lo, int64_t sec_len, int vec_ok, uint32_t* __restrict__ flag) {
+  constexpr int E = Unit16B<BITS>::E;
+  constexpr int U = 2;
+  constexpr int QMAX = Codes<BITS>::kQmax;
+  constexpr float RQ = 1.0f / QMAX;
+  const int lane = threadIdx.x & 31;
+  const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarp = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t units = (shard_len + E - 1) / E;
+  const int64_t tiles = (units + 32 * U - 1) / (32 * U);
+  const int64_t n_tiles = tiles * n_src;
+  const bool pow2 = (B & (B - 1)) == 0;
+  const int lg = pow2 ? __ffsll(B) - 1 : 0;
+  bool bad = false;
+  for (int64_t tile = gwarp; tile < n_tiles; tile += nwarp) {
+    const int s = (int)((tile % n_src + rot) % n_src);
+    const int64_t t0 = (tile / n_src) * 32 * U;
+    uint4 w[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t unit = t0 + u * 32 + lane;
+      w[u] = unit < units ? __ldg(reinterpret_cast<const uint4*>(src.codes[s]) + unit) : make_uint4(0, 0, 0, 0);
+    }
+    const float* am = reinterpret_cast<const float*>(src.absmax[s]);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t unit = t0 + u * 32 + lane;
+      if (unit >= units) continue;
+      bad |= bad_codes(w[u], BITS);
+      const int64_t e0 = unit * E;
+      const float m = __ldg(am + (pow2 ? (e0 >> lg) : e0 / B));
+      const float s32 = __fmul_rn(m, RQ);
+      // exact16: absmax fits the output format's significand (fp16-sourced
+      // scales for fp16 output, bf16-sourced for bf16/fp16).  Then
+      // z = code*absmax/qmax is either representable or a rational whose
+      // distance to every output rounding midpoint is >= 2^-(p+1)/qmax
+      // relative (p = 11 or 8 significand bits; qmax prime), while the fp32
+      // product below is within 1.5*2^-23 of z and RN64(z) within 2^-52: both
+      // round to the same 16-bit value, so no per-element check is needed.
+      const bool exact16 = ((__float_as_uint(m) & Out16<O>::kLowMask) == 0u) && Out16<O>::in_range(m);
+      const bool sok = Out16<O>::scale_ok(s32, QMAX);
+      const uint32_t wa[4] = {w[u].x, w[u].y, w[u].z, w[u].w};
+      // two halves of HE elements (2 code words each)
+#pragma unroll
+      for (int hf = 0; hf < 2; ++hf) {
+        constexpr int HE = E / 2;
+        const int64_t eh = e0 + hf * HE;
+        const int cnt = (int)max((int64_t)0, min((int64_t)HE, shard_len - eh));
+        if (cnt == 0) continue;
+        uint32_t h[HE / 2];
+        uint32_t risky = (exact16 || sok) ? 0xFFFFFFFFu : 0u;
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          uint32_t f[32 / BITS];
+          magic_word<BITS>(wa[2 * hf + i], f);
+#pragma unroll
+          for (int j = 0; j < 32 / BITS; j += 2) {
+            const float2 c = fadd2(make_float2(__uint_as_float(f[j]), __uint_as_float(f[j + 1])),
+                                   make_float2(-Bias<BITS>::kF, -Bias<BITS>::kF));
+            const float2 p = fmul2(c, make_float2(s32, s32));
+            if (!exact16)
+              risky = min(risky, min(Out16<O>::near_mid(__float_as_uint(p.x)), Out16<O>::near_mid(__float_as_uint(p.y))));
+            h[(i * (32 / BITS) + j) / 2] = Out16<O>::pack2(p.x, p.y);
+          }
+        }
+        if (risky == 0u) {  // rare (fp32-sourced scales only): exact f64 path for this half unit
+          const double s64 = scale_of<BITS>((double)m);
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            uint32_t f[32 / BITS];
+            magic_word<BITS>(wa[2 * hf + i], f);
+#pragma unroll
+            for (int j = 0; j < 32 / BITS; j += 2) {
+              O a = from_f64<O>(__dmul_rn(code_f64<BITS>(f[j]), s64));
+              O b = from_f64<O>(__dmul_rn(code_f64<BITS>(f[j + 1]), s64));
+              h[(i * (32 / BITS) + j) / 2] =
+                  (uint32_t)(*reinterpret_cast<uint16_t*>(&a)) | ((uint32_t)(*reinterpret_cast<uint16_t*>(&b)) << 16);
+            }
+          }
+        }
+        const int64_t oi = (int64_t)s * shard_len + eh;
+        O* dst = out + oi;
+        if (vec_ok && cnt == HE) {
+#pragma unroll
+          for (int i = 0; i < HE / 8; ++i)
+            reinterpret_cast<uint4*>(dst)[i] = make_uint4(h[4 * i], h[4 * i + 1], h[4 * i + 2], h[4 * i + 3]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < HE; ++i)
+            if (i < cnt) store_scalar<O>(dst, i, h[i / 2] >> (16 * (i & 1)));
+        }
+        if (sec_out != nullptr && oi + cnt > sec_lo && oi < sec_lo + sec_len) {
+          const int64_t k0 = oi - sec_lo;
+          if (vec_ok && cnt == HE && k0 >= 0 && k0 + HE <= sec_len) {
+#pragma unroll
+            for (int i = 0; i < HE / 8; ++i)
+              reinterpret_cast<uint4*>(sec_out + k0)[i] = make_uint4(h[4 * i], h[4 * i + 1], h[4 * i + 2], h[4 * i + 3]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < HE; ++i)
+              if (i < cnt && k0 + i >= 0 && k0 + i < sec_len)
+                store_scalar<O>(sec_out + k0, i, h[i / 2] >> (16 * (i & 1)));
+          }
+        }
+      }
+    }
+  }
+  if (bad) raise_flag(flag, FLAG_BADCODE);
+}
+
+// ---------------------------------------------------------------------------
+// exact (f64) decode of 8-element chunks, for fp32/f64 outputs, f64 absmax,
+// odd block sizes and odd alignments
 
 template <int BITS>
 __device__ __forceinline__ void decode8(const uint8_t* p, double s, double (&v)[8], bool& bad) {
   if constexpr (BITS == 8) {
     uint2 w = *reinterpret_cast<const uint2*>(p);
     bad |= has_byte_0x80(w.x) | has_byte_0x80(w.y);
-    uint32_t u[4];
-    constexpr double mb = kMagic52 + 128.0;
-    unpack4_int8(w.x, u);
+    uint32_t f[4];
+    magic_int8(w.x, f);
 #pragma unroll
-    for (int i = 0; i < 4; ++i) v[i] = __dmul_rn(biased_to_f64(u[i], mb), s);
-    unpack4_int8(w.y, u);
+    for (int i = 0; i < 4; ++i) v[i] = __dmul_rn(code_f64<8>(f[i]), s);
+    magic_int8(w.y, f);
 #pragma unroll
-    for (int i = 0; i < 4; ++i) v[4 + i] = __dmul_rn(biased_to_f64(u[i], mb), s);
+    for (int i = 0; i < 4; ++i) v[4 + i] = __dmul_rn(code_f64<8>(f[i]), s);
   } else {
     uint32_t w = *reinterpret_cast<const uint32_t*>(p);
     bad |= has_nibble_8(w);
-    uint32_t u[8];
-    constexpr double mb = kMagic52 + 8.0;
-    unpack8_int4(w, u);
+    uint32_t f[8];
+    magic_int4(w, f);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) v[i] = __dmul_rn(biased_to_f64(u[i], mb), s);
+    for (int i = 0; i < 8; ++i) v[i] = __dmul_rn(code_f64<4>(f[i]), s);
   }
 }
 
@@ -402,11 +667,10 @@ __device__ __forceinline__ void store8(O* dst, const double (&v)[8], int cnt, bo
       }
       *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
     } else if constexpr (sizeof(O) == 4) {
-      float f[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) f[i] = from_f64<float>(v[i]);
-      reinterpret_cast<float4*>(dst)[0] = make_float4(f[0], f[1], f[2], f[3]);
-      reinterpret_cast<float4*>(dst)[1] = make_float4(f[4], f[5], f[6], f[7]);
+      reinterpret_cast<float4*>(dst)[0] = make_float4(from_f64<float>(v[0]), from_f64<float>(v[1]),
+                                                      from_f64<float>(v[2]), from_f64<float>(v[3]));
+      reinterpret_cast<float4*>(dst)[1] = make_float4(from_f64<float>(v[4]), from_f64<float>(v[5]),
+                                                      from_f64<float>(v[6]), from_f64<float>(v[7]));
     } else {
 #pragma unroll
       for (int i = 0; i < 4; ++i) reinterpret_cast<double2*>(dst)[i] = make_double2(v[2 * i], v[2 * i + 1]);
@@ -418,47 +682,50 @@ __device__ __forceinline__ void store8(O* dst, const double (&v)[8], int cnt, bo
   }
 }
 
-// ---------------------------------------------------------------------------
-// K4: dequantize / gather-dequantize.  Output = concatenation of the n_src
-// sources' decoded shards (shard_len each), the qwZ receive side
-// (zs/collectives.py:264).  Warps walk 32-chunk groups with the source index
-// fastest-varying and rotated by `rot`, so at any moment every peer's NVLink
-// egress is being read.  Optional hpZ write-through: output range
-// [sec_lo, sec_lo + sec_len) is also written to sec_out (the secondary
-// partition, zs/engine.py:364-367).
-
+// K4 exact path: 8-element chunks, U chunks per lane per iteration (loads first)
 template <int BITS, typename A, typename O>
 __global__ void __launch_bounds__(256)
 dequant_gather_kernel(SrcTable src, int n_src, int rot, int64_t shard_len, int64_t B, O* __restrict__ out,
                       O* __restrict__ sec_out, int64_t sec_lo, int64_t sec_len, int vec_ok,
                       uint32_t* __restrict__ flag) {
+  constexpr int U = 4;
+  using CW = typename std::conditional<BITS == 8, uint2, uint32_t>::type;
   const int lane = threadIdx.x & 31;
   const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarp = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t chunks = (shard_len + 7) / 8;
-  const int64_t groups_per_src = (chunks + 31) / 32;
-  const int64_t n_groups = groups_per_src * n_src;
+  const int64_t tiles = (chunks + 32 * U - 1) / (32 * U);
+  const int64_t n_tiles = tiles * n_src;
   const bool pow2 = (B & (B - 1)) == 0;
   const int lg = pow2 ? __ffsll(B) - 1 : 0;
   bool bad = false;
-  for (int64_t g = gwarp; g < n_groups; g += nwarp) {
-    int s = (int)(g % n_src);
-    s = (s + rot) % n_src;
-    const int64_t ch = (g / n_src) * 32 + lane;
-    if (ch >= chunks) continue;
-    const int64_t e = ch * 8;
-    const int64_t blk = pow2 ? (e >> lg) : e / B;
-    const double sc = scale_of<BITS>(absmax_f64<A>(reinterpret_cast<const A*>(src.absmax[s]), blk));
-    double v[8];
-    decode8<BITS>(src.codes[s] + ch * BITS, sc, v, bad);
-    const int cnt = (int)min((int64_t)8, shard_len - e);
-    const int64_t oi = (int64_t)s * shard_len + e;
-    store8<O>(out + oi, v, cnt, vec_ok);
-    if (sec_out != nullptr && oi + cnt > sec_lo && oi < sec_lo + sec_len) {
+  for (int64_t tile = gwarp; tile < n_tiles; tile += nwarp) {
+    const int s = (int)((tile % n_src + rot) % n_src);
+    const int64_t t0 = (tile / n_src) * 32 * U;
+    const A* am = reinterpret_cast<const A*>(src.absmax[s]);
+    CW w[U];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int64_t k = oi + i - sec_lo;
-        if (i < cnt && k >= 0 && k < sec_len) sec_out[k] = from_f64<O>(v[i]);
+    for (int u = 0; u < U; ++u) {
+      const int64_t ch = t0 + u * 32 + lane;
+      w[u] = ch < chunks ? __ldg(reinterpret_cast<const CW*>(src.codes[s] + ch * BITS)) : CW{};
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t ch = t0 + u * 32 + lane;
+      if (ch >= chunks) continue;
+      const int64_t e = ch * 8;
+      const double sc = scale_of<BITS>(absmax_f64<A>(am, pow2 ? (e >> lg) : e / B));
+      double v[8];
+      decode8<BITS>(reinterpret_cast<const uint8_t*>(&w[u]), sc, v, bad);
+      const int cnt = (int)min((int64_t)8, shard_len - e);
+      const int64_t oi = (int64_t)s * shard_len + e;
+      store8<O>(out + oi, v, cnt, vec_ok);
+      if (sec_out != nullptr && oi + cnt > sec_lo && oi < sec_lo + sec_len) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int64_t k = oi + i - sec_lo;
+          if (i < cnt && k >= 0 && k < sec_len) sec_out[k] = from_f64<O>(v[i]);
+        }
       }
     }
   }
@@ -468,89 +735,141 @@ dequant_gather_kernel(SrcTable src, int n_src, int rot, int64_t shard_len, int64
 // ---------------------------------------------------------------------------
 // K3: dequantize n_src sources of n elements each and fold them in f64 from
 // +0.0 in source order; optional f64 post-scale (1.0 = the reference's sum).
+// Lane unit: 8-element chunk; each lane owns 2 chunks per iteration and issues
+// the code loads of up to 4 sources before decoding them.
 
 template <int BITS, typename A, typename O>
 __global__ void __launch_bounds__(256)
 dequant_reduce_kernel(SrcTable src, int n_src, int64_t n, int64_t B, O* __restrict__ out, double post_scale,
                       int vec_ok, uint32_t* __restrict__ flag) {
+  constexpr int U = 2;
+  constexpr int SB = 4;
+  using CW = typename std::conditional<BITS == 8, uint2, uint32_t>::type;
+  const int lane = threadIdx.x & 31;
+  const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarp = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t chunks = (n + 7) / 8;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t tiles = (chunks + 32 * U - 1) / (32 * U);
   const bool pow2 = (B & (B - 1)) == 0;
   const int lg = pow2 ? __ffsll(B) - 1 : 0;
   bool bad = false;
-  for (int64_t ch = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; ch < chunks; ch += stride) {
-    const int64_t e = ch * 8;
-    const int64_t blk = pow2 ? (e >> lg) : e / B;
-    double acc[8];
+  for (int64_t tile = gwarp; tile < tiles; tile += nwarp) {
+    const int64_t t0 = tile * 32 * U;
+    double acc[U][8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) acc[i] = 0.0;
-    for (int s = 0; s < n_src; ++s) {
-      const double sc = scale_of<BITS>(absmax_f64<A>(reinterpret_cast<const A*>(src.absmax[s]), blk));
-      decode8_acc<BITS>(src.codes[s] + ch * BITS, sc, acc, bad);
-    }
-    if (post_scale != 1.0) {
+    for (int u = 0; u < U; ++u)
 #pragma unroll
-      for (int i = 0; i < 8; ++i) acc[i] = __dmul_rn(acc[i], post_scale);
+      for (int i = 0; i < 8; ++i) acc[u][i] = 0.0;
+    for (int s0 = 0; s0 < n_src; s0 += SB) {
+      CW w[SB][U];
+#pragma unroll
+      for (int j = 0; j < SB; ++j)
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int64_t ch = t0 + u * 32 + lane;
+          if (s0 + j < n_src && ch < chunks)
+            w[j][u] = __ldg(reinterpret_cast<const CW*>(src.codes[s0 + j] + ch * BITS));
+          else
+            w[j][u] = CW{};
+        }
+#pragma unroll
+      for (int j = 0; j < SB; ++j) {
+        if (s0 + j >= n_src) break;
+        const A* am = reinterpret_cast<const A*>(src.absmax[s0 + j]);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int64_t ch = t0 + u * 32 + lane;
+          if (ch >= chunks) continue;
+          const int64_t e = ch * 8;
+          const double sc = scale_of<BITS>(absmax_f64<A>(am, pow2 ? (e >> lg) : e / B));
+          decode8_acc<BITS>(reinterpret_cast<const uint8_t*>(&w[j][u]), sc, acc[u], bad);
+        }
+      }
     }
-    store8<O>(out + e, acc, (int)min((int64_t)8, n - e), vec_ok);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t ch = t0 + u * 32 + lane;
+      if (ch >= chunks) continue;
+      const int64_t e = ch * 8;
+      if (post_scale != 1.0) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[u][i] = __dmul_rn(acc[u][i], post_scale);
+      }
+      store8<O>(out + e, acc[u], (int)min((int64_t)8, n - e), vec_ok);
+    }
   }
   if (bad) raise_flag(flag, FLAG_BADCODE);
 }
 
 // ---------------------------------------------------------------------------
 // K2 register path: a team of LANES lanes owns one OUTPUT block of
-// B2 = LANES * EPL elements; for each source (ascending) it dequantizes the
-// 8-element chunks (input block size B1 arbitrary) and folds them into f64
-// accumulators, then requantizes from the exact f64 block absmax.  The output
-// absmax is stored in f64, so the next hop decodes bit-exactly.
+// B2 = LANES * 16 elements (lane = 16 contiguous elements = two 8-chunks).
+// For each source (ascending, loads of up to 4 sources in flight) the codes
+// are dequantized (input block size B1 arbitrary, multiple of 8) and folded
+// into f64 accumulators; then the block is requantized from its exact f64
+// absmax, which is stored in f64 so the next hop decodes bit-exactly.
 
-template <int IBITS, typename IA, int OBITS, int LANES, int EPL>
+template <int IBITS, typename IA, int OBITS, int LANES>
 __global__ void __launch_bounds__(256)
 drq_reg_kernel(SrcTable src, int n_src, int64_t n, int64_t B1, int64_t n_blocks_out, uint8_t* __restrict__ codes,
                double* __restrict__ absmax, uint32_t* __restrict__ flag) {
-  constexpr int B2 = LANES * EPL;
-  constexpr int CH = EPL / 8;
+  constexpr int B2 = LANES * 16;
   constexpr int TPW = 32 / LANES;
   constexpr int QMAX = Codes<OBITS>::kQmax;
+  constexpr int SB = 4;
+  using CW = typename std::conditional<IBITS == 8, uint2, uint32_t>::type;  // one 8-chunk of codes
   const int lane = threadIdx.x & 31;
   const int tl = lane % LANES;
+  const int team = lane / LANES;
   const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarp = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const bool pow2 = (B1 & (B1 - 1)) == 0;
   const int lg = pow2 ? __ffsll(B1) - 1 : 0;
+  const int64_t chunks_in = (n + B1 - 1) / B1 * B1 / 8;  // padded input chunks
   bool bad = false;
   for (int64_t wb = gwarp * TPW; wb < n_blocks_out; wb += nwarp * TPW) {
-    const int64_t b = wb + lane / LANES;
+    const int64_t b = wb + team;
     const bool active = b < n_blocks_out;
-    double acc[CH][8];
+    const int64_t c0 = (b * B2 + (int64_t)tl * 16) / 8;  // first of this lane's two chunks
+    double acc[2][8];
 #pragma unroll
-    for (int c = 0; c < CH; ++c)
+    for (int h = 0; h < 2; ++h)
 #pragma unroll
-      for (int i = 0; i < 8; ++i) acc[c][i] = 0.0;
-    for (int s = 0; s < n_src; ++s) {
-      const IA* am = reinterpret_cast<const IA*>(src.absmax[s]);
+      for (int i = 0; i < 8; ++i) acc[h][i] = 0.0;
+    for (int s0 = 0; s0 < n_src; s0 += SB) {
+      CW w[SB][2];
 #pragma unroll
-      for (int c = 0; c < CH; ++c) {
-        const int64_t e = b * B2 + (c * LANES + tl) * 8;
-        if (active && e < n) {
-          const int64_t ib = pow2 ? (e >> lg) : e / B1;
-          const double sc = scale_of<IBITS>(absmax_f64<IA>(am, ib));
-          decode8_acc<IBITS>(src.codes[s] + (e / 8) * IBITS, sc, acc[c], bad);
+      for (int j = 0; j < SB; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int64_t ch = c0 + h;
+          if (active && s0 + j < n_src && ch < chunks_in)
+            w[j][h] = __ldg(reinterpret_cast<const CW*>(src.codes[s0 + j] + ch * IBITS));
+          else
+            w[j][h] = CW{};
+        }
+#pragma unroll
+      for (int j = 0; j < SB; ++j) {
+        if (s0 + j >= n_src) break;
+        const IA* am = reinterpret_cast<const IA*>(src.absmax[s0 + j]);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int64_t ch = c0 + h;
+          if (!active || ch >= chunks_in) continue;
+          const int64_t e = ch * 8;
+          const double sc = scale_of<IBITS>(absmax_f64<IA>(am, pow2 ? (e >> lg) : e / B1));
+          decode8_acc<IBITS>(reinterpret_cast<const uint8_t*>(&w[j][h]), sc, acc[h], bad);
         }
       }
     }
-    // n is a multiple of 8 except possibly in the generic fused API; zero the
-    // tail of a partial chunk like the reference's zero padding
     double mx = 0.0;
 #pragma unroll
-    for (int c = 0; c < CH; ++c) {
-      const int64_t e = b * B2 + (c * LANES + tl) * 8;
+    for (int h = 0; h < 2; ++h)
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        if (e + i >= n) acc[c][i] = 0.0;
-        mx = fmax(mx, fabs(acc[c][i]));
+        if ((c0 + h) * 8 + i >= n) acc[h][i] = 0.0;  // zero padding like the reference
+        mx = fmax(mx, fabs(acc[h][i]));
       }
-    }
 #pragma unroll
     for (int off = LANES / 2; off >= 1; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
     if (active && tl == 0) {
@@ -559,13 +878,18 @@ drq_reg_kernel(SrcTable src, int n_src, int64_t n, int64_t B1, int64_t n_blocks_
     }
     const double inv = mx > 0.0 ? __ddiv_rn((double)QMAX, mx) : 0.0;
     if (active) {
-      uint8_t* out = codes + b * (int64_t)(B2 * OBITS / 8);
+      uint32_t q0[8], q1[8];
 #pragma unroll
-      for (int c = 0; c < CH; ++c) {
-        uint32_t q[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) q[i] = q_exact<QMAX>(acc[c][i], inv);
-        store_codes8<OBITS>(out + (c * LANES + tl) * OBITS, q);
+      for (int i = 0; i < 8; ++i) {
+        q0[i] = q_exact<QMAX>(acc[0][i], inv);
+        q1[i] = q_exact<QMAX>(acc[1][i], inv);
+      }
+      uint8_t* dst = codes + c0 * OBITS;
+      if constexpr (OBITS == 8) {
+        const uint2 a = pack8_int8(q0), c = pack8_int8(q1);
+        *reinterpret_cast<uint4*>(dst) = make_uint4(a.x, a.y, c.x, c.y);
+      } else {
+        *reinterpret_cast<uint2*>(dst) = make_uint2(pack8_int4(q0), pack8_int4(q1));
       }
     }
   }

@@ -183,7 +183,10 @@ def test_div_by_qmax_exhaustive_fp32():
         for b, qm in ((8, 127.0), (4, 7.0)):
             zpp._lib.check(lib.zpp_scales(m.data_ptr(), zpp._lib.F32, cnt, b, out.data_ptr(),
                                           torch.cuda.current_stream().cuda_stream))
-            want = m.double() / qm
+            md = m.double()
+            # tensor / tensor: torch turns `tensor / python_scalar` into a
+            # reciprocal multiply, which is not IEEE division
+            want = md / torch.full_like(md, qm)
             assert torch.equal(out[:cnt], want), (start, b)
 
 
@@ -198,7 +201,7 @@ def test_div_by_qmax_random_f64():
         for b, qm in ((8, 127.0), (4, 7.0)):
             zpp._lib.check(lib.zpp_scales(m.data_ptr(), zpp._lib.F64, m.numel(), b, out.data_ptr(),
                                           torch.cuda.current_stream().cuda_stream))
-            assert torch.equal(out, m / qm)
+            assert torch.equal(out, m / torch.full_like(m, qm))
 
 
 def test_config1_full_size_roundtrip():
@@ -254,3 +257,30 @@ def test_error_bound_half_scale():
         x = torch.randn(20000, dtype=torch.float64, device="cuda") * 10
         st = zpp.quant_error_stats(x, zpp.QuantConfig(bit_width=bits, block_size=512))
         assert st.per_block_bound_violations == 0 and st.max_abs_error > 0
+
+
+@pytest.mark.parametrize("src", ["fp16", "bf16", "fp32"])
+@pytest.mark.parametrize("bits,block", [(8, 2048), (4, 512), (8, 64)])
+def test_dequant16_fast_path_bit_exact_stress(src, bits, block):
+    """4M heavy-tailed values per case through the 16-bit-output kernels
+    (scale-bit-width proof path for fp16/bf16 sources, checked path for fp32
+    sources): every fp16 / bf16 output equals the reference's f64 rounded once."""
+    zpp = _zpp()
+    rng = np.random.default_rng(hash((src, bits, block)) % 2**32)
+    n = 1 << 22
+    v = np.clip(rng.normal(size=n) * np.exp(rng.normal(size=n) * 3), -6e4, 6e4)
+    if src == "fp16":
+        arr = v.astype(np.float16)
+    elif src == "bf16":
+        arr = (v.astype(np.float32).view(np.uint32) >> 16).astype(np.uint16)
+    else:
+        arr = v.astype(np.float32)
+    q = zpp.quantize(gu.to_torch(arr, src), zpp.QuantConfig(bit_width=bits, block_size=block))
+    c, s, _ = O.quantize(gu.as_f64(arr, src), bits, block)
+    assert np.array_equal(q.codes.cpu().numpy(), c)
+    ref = O.dequantize(c, s, n, bits, block)
+    for dt, name in [(torch.float16, "fp16"), (torch.bfloat16, "bf16")]:
+        got = zpp.dequantize(q, dt).values.to(torch.float64).cpu().numpy()
+        want = gu.round_to(ref, name)
+        bad = np.flatnonzero(~((got == want) | (np.isnan(got) & np.isnan(want))))
+        assert bad.size == 0, (name, bad[:5], got[bad[:5]], want[bad[:5]])

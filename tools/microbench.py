@@ -42,11 +42,17 @@ def report(name, sec, nbytes):
 
 
 def main():
+    only = sys.argv[1] if len(sys.argv) > 1 else "all"
     lib = _lib.load()
     st = torch.cuda.current_stream().cuda_stream
     flag = torch.zeros(1, dtype=torch.int32, device="cuda")
-    for (dt, n, bits, block) in [(torch.float16, 1_300_004_864, 8, 2048), (torch.float32, 1 << 24, 8, 2048),
-                                 (torch.bfloat16, 134_217_728, 4, 512), (torch.float16, 134_217_728, 8, 2048)]:
+    cases = [(torch.float16, 1_300_004_864, 8, 2048), (torch.float32, 1 << 24, 8, 2048),
+             (torch.bfloat16, 134_217_728, 4, 512), (torch.float16, 134_217_728, 8, 2048)]
+    if only == "qgz":
+        cases = []
+    elif only == "codec":
+        cases = cases[2:4]
+    for (dt, n, bits, block) in cases:
         x = (torch.randn(n, device="cuda", dtype=torch.float32) * 0.02).to(dt)
         q = zpp.quantize(x, zpp.QuantConfig(bit_width=bits, block_size=block))
         code = zpp.quantizer.dtype_code(dt)
@@ -69,6 +75,8 @@ def main():
             del out
         del x, q
         torch.cuda.empty_cache()
+    if only == "codec":
+        return
     # qgZ kernels at the W=8 bucket shape, emulated on one GPU (X=4, Y=2)
     n = 134_217_728
     g = (torch.randn(n, device="cuda") * 1e-3).bfloat16()
