@@ -182,7 +182,7 @@ static int run_gather(const SrcTable& t, int n_src, int rot, int64_t shard_len, 
     for (int i = 0; i < n_src; ++i) fast = fast && aligned16(t.codes[i]);
     if (fast) {
       auto k = dequant16_kernel<BITS, O>;
-      const int64_t tiles = ceil_div(ceil_div(shard_len, 128 / BITS), 32 * 2) * n_src;
+      const int64_t tiles = ceil_div(ceil_div(shard_len, 128 / BITS), 32 * (BITS == 8 ? 2 : 1)) * n_src;
       const int grid = grid_for(k, 256, ceil_div(tiles, 8));
       k<<<grid, 256, 0, st>>>(t, n_src, rot, shard_len, block, reinterpret_cast<O*>(out),
                               reinterpret_cast<O*>(sec_out), sec_lo, sec_len, vec_ok, flag);

@@ -252,14 +252,20 @@ quantize_reg_kernel(const T* __restrict__ x, Addr addr, int64_t n_blocks, uint8_
     }
     uint32_t raw[CH][RW];
     uint32_t acc = 0;
+    if (active && valid >= B) {  // full block: unconditional vector loads
+      const T* xb = x + src + tl * 8;
 #pragma unroll
-    for (int c = 0; c < CH; ++c) {
-      const int e = (c * LANES + tl) * 8;
-      if (active && e + 8 <= valid) {
-        Raw<T>::load(x + src + e, raw[c]);
-      } else {
-        const int cnt = active ? (int)max((int64_t)0, min((int64_t)8, valid - e)) : 0;
-        Raw<T>::load_scalar(x + src + e, cnt, raw[c]);
+      for (int c = 0; c < CH; ++c) Raw<T>::load(xb + c * LANES * 8, raw[c]);
+    } else {
+#pragma unroll
+      for (int c = 0; c < CH; ++c) {
+        const int e = (c * LANES + tl) * 8;
+        if (active && e + 8 <= valid) {
+          Raw<T>::load(x + src + e, raw[c]);
+        } else {
+          const int cnt = active ? (int)max((int64_t)0, min((int64_t)8, valid - e)) : 0;
+          Raw<T>::load_scalar(x + src + e, cnt, raw[c]);
+        }
       }
     }
 #pragma unroll
@@ -273,8 +279,8 @@ quantize_reg_kernel(const T* __restrict__ x, Addr addr, int64_t n_blocks, uint8_
       if (Raw<T>::nonfinite(mb)) raise_flag(flag, FLAG_NONFINITE);
     }
     const float inv32 = m > 0.0f ? __fdiv_rn((float)QMAX, m) : 0.0f;
-    const double inv64 = m > 0.0f ? __ddiv_rn((double)QMAX, (double)m) : 0.0;
     const bool slow = !(inv32 <= 0x1p100f);  // reciprocal of a (sub)normal tiny absmax
+    const double inv64 = m > 0.0f ? __ddiv_rn((double)QMAX, (double)m) : 0.0;
     uint8_t* out = codes + b * (int64_t)(B * BITS / 8);
 #pragma unroll
     for (int c = 0; c < CH; ++c) {
@@ -508,112 +514,143 @@ __device__ __forceinline__ void store_scalar(O* dst, int i, uint32_t bits16) {
 // Optional hpZ write-through of output range [sec_lo, sec_lo+sec_len) into
 // sec_out (the secondary partition, zs/engine.py:364-367).
 
+// decode one 16-byte unit (E elements) into packed 16-bit outputs h[E/2].
+// CHECKED = false: the exact16 proof applies, pure packed fp32 math.
+// CHECKED = true : per-element midpoint test with an exact f64 redo.
+template <int BITS, typename O, bool CHECKED>
+__device__ __forceinline__ void decode16_unit(uint4 w, float m, float s32, uint32_t (&h)[Unit16B<BITS>::E / 2]) {
+  const uint32_t wa[4] = {w.x, w.y, w.z, w.w};
+  uint32_t risky = 0xFFFFFFFFu;
+  if constexpr (CHECKED) risky = Out16<O>::scale_ok(s32, Codes<BITS>::kQmax) ? 0xFFFFFFFFu : 0u;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    uint32_t f[32 / BITS];
+    magic_word<BITS>(wa[i], f);
+#pragma unroll
+    for (int j = 0; j < 32 / BITS; j += 2) {
+      const float2 c = fadd2(make_float2(__uint_as_float(f[j]), __uint_as_float(f[j + 1])),
+                             make_float2(-Bias<BITS>::kF, -Bias<BITS>::kF));
+      const float2 p = fmul2(c, make_float2(s32, s32));
+      if constexpr (CHECKED)
+        risky = min(risky, min(Out16<O>::near_mid(__float_as_uint(p.x)), Out16<O>::near_mid(__float_as_uint(p.y))));
+      h[(i * (32 / BITS) + j) / 2] = Out16<O>::pack2(p.x, p.y);
+    }
+  }
+  if constexpr (CHECKED) {
+    if (risky == 0u) {  // exact f64 redo of this unit
+      const double s64 = scale_of<BITS>((double)m);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        uint32_t f[32 / BITS];
+        magic_word<BITS>(wa[i], f);
+#pragma unroll
+        for (int j = 0; j < 32 / BITS; j += 2) {
+          O a = from_f64<O>(__dmul_rn(code_f64<BITS>(f[j]), s64));
+          O b = from_f64<O>(__dmul_rn(code_f64<BITS>(f[j + 1]), s64));
+          h[(i * (32 / BITS) + j) / 2] =
+              (uint32_t)(*reinterpret_cast<uint16_t*>(&a)) | ((uint32_t)(*reinterpret_cast<uint16_t*>(&b)) << 16);
+        }
+      }
+    }
+  }
+}
+
+// exact16: absmax fits the output format's significand (fp16-sourced scales
+// for fp16 output, bf16-sourced for bf16/fp16).  Then z = code*absmax/qmax is
+// either representable or a rational whose distance to every output rounding
+// midpoint is >= 2^-(p+1)/qmax relative (p = 11 or 8 significand bits; qmax
+// prime), while the fp32 product is within 1.5*2^-23 of z and RN64(z) within
+// 2^-52: both round to the same 16-bit value, so no per-element check.
 template <int BITS, typename O>
-__global__ void __launch_bounds__(256)
+__device__ __forceinline__ void decode16_any(uint4 w, float m, uint32_t (&h)[Unit16B<BITS>::E / 2]) {
+  constexpr float RQ = 1.0f / Codes<BITS>::kQmax;
+  const float s32 = __fmul_rn(m, RQ);
+  if (((__float_as_uint(m) & Out16<O>::kLowMask) == 0u) && Out16<O>::in_range(m))
+    decode16_unit<BITS, O, false>(w, m, s32, h);
+  else
+    decode16_unit<BITS, O, true>(w, m, s32, h);
+}
+
+template <int N>
+__device__ __forceinline__ void store_words(void* dst, const uint32_t (&h)[N]) {
+#pragma unroll
+  for (int i = 0; i < N / 4; ++i)
+    reinterpret_cast<uint4*>(dst)[i] = make_uint4(h[4 * i], h[4 * i + 1], h[4 * i + 2], h[4 * i + 3]);
+}
+
+template <int BITS, typename O>
+__global__ void __launch_bounds__(256, 4)
 dequant16_kernel(SrcTable src, int n_src, int rot, int64_t shard_len, int64_t B, O* __restrict__ out,
                  O* __restrict__ sec_out, int64_t sec_lo, int64_t sec_len, int vec_ok, uint32_t* __restrict__ flag) {
   constexpr int E = Unit16B<BITS>::E;
-  constexpr int U = 2;
-  constexpr int QMAX = Codes<BITS>::kQmax;
-  constexpr float RQ = 1.0f / QMAX;
+  constexpr int U = BITS == 8 ? 2 : 1;  // 16-byte code loads per lane per tile
+  constexpr int TU = 32 * U;            // units per warp tile
   const int lane = threadIdx.x & 31;
-  const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarp = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int64_t units = (shard_len + E - 1) / E;
-  const int64_t tiles = (units + 32 * U - 1) / (32 * U);
-  const int64_t n_tiles = tiles * n_src;
+  const int gwarp = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int nwarp = (int)(((int64_t)gridDim.x * blockDim.x) >> 5);
+  const int units = (int)((shard_len + E - 1) / E);
+  const int full_units = vec_ok ? (int)(shard_len / E) : 0;
+  const int tiles = (units + TU - 1) / TU;
+  const int n_tiles = tiles * n_src;
   const bool pow2 = (B & (B - 1)) == 0;
   const int lg = pow2 ? __ffsll(B) - 1 : 0;
   bool bad = false;
-  for (int64_t tile = gwarp; tile < n_tiles; tile += nwarp) {
-    const int s = (int)((tile % n_src + rot) % n_src);
-    const int64_t t0 = (tile / n_src) * 32 * U;
-    uint4 w[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t unit = t0 + u * 32 + lane;
-      w[u] = unit < units ? __ldg(reinterpret_cast<const uint4*>(src.codes[s]) + unit) : make_uint4(0, 0, 0, 0);
-    }
+  for (int g = gwarp; g < n_tiles; g += nwarp) {
+    const int t = g / n_src;
+    int s = g - t * n_src + rot;
+    if (s >= n_src) s -= n_src;
+    const int t0 = t * TU;
+    const uint4* cs = reinterpret_cast<const uint4*>(src.codes[s]);
     const float* am = reinterpret_cast<const float*>(src.absmax[s]);
+    const int64_t obase = (int64_t)s * shard_len;
+    // tile fully inside the shard, vector-aligned and not touching the hpZ
+    // secondary range: branch-free fast path
+    const int64_t te0 = obase + (int64_t)t0 * E, te1 = te0 + (int64_t)TU * E;
+    const bool sec_touch = sec_out != nullptr && te1 > sec_lo && te0 < sec_lo + sec_len;
+    if (t0 + TU <= full_units && !sec_touch) {
+      uint4 w[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) w[u] = __ldg(cs + t0 + u * 32 + lane);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int unit = t0 + u * 32 + lane;
+        bad |= bad_codes(w[u], BITS);
+        const int64_t e0 = (int64_t)unit * E;
+        const float m = __ldg(am + (pow2 ? (e0 >> lg) : e0 / B));
+        uint32_t h[E / 2];
+        decode16_any<BITS, O>(w[u], m, h);
+        store_words<E / 2>(out + obase + e0, h);
+      }
+      continue;
+    }
+    // edge tiles: bounds, partial units, scalar stores, hpZ write-through
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int64_t unit = t0 + u * 32 + lane;
+      const int unit = t0 + u * 32 + lane;
       if (unit >= units) continue;
-      bad |= bad_codes(w[u], BITS);
-      const int64_t e0 = unit * E;
+      const uint4 w = __ldg(cs + unit);
+      bad |= bad_codes(w, BITS);
+      const int64_t e0 = (int64_t)unit * E;
       const float m = __ldg(am + (pow2 ? (e0 >> lg) : e0 / B));
-      const float s32 = __fmul_rn(m, RQ);
-      // exact16: absmax fits the output format's significand (fp16-sourced
-      // scales for fp16 output, bf16-sourced for bf16/fp16).  Then
-      // z = code*absmax/qmax is either representable or a rational whose
-      // distance to every output rounding midpoint is >= 2^-(p+1)/qmax
-      // relative (p = 11 or 8 significand bits; qmax prime), while the fp32
-      // product below is within 1.5*2^-23 of z and RN64(z) within 2^-52: both
-      // round to the same 16-bit value, so no per-element check is needed.
-      const bool exact16 = ((__float_as_uint(m) & Out16<O>::kLowMask) == 0u) && Out16<O>::in_range(m);
-      const bool sok = Out16<O>::scale_ok(s32, QMAX);
-      const uint32_t wa[4] = {w[u].x, w[u].y, w[u].z, w[u].w};
-      // two halves of HE elements (2 code words each)
+      uint32_t h[E / 2];
+      decode16_any<BITS, O>(w, m, h);
+      const int cnt = (int)min((int64_t)E, shard_len - e0);
+      const int64_t oi = obase + e0;
+      if (vec_ok && cnt == E) {
+        store_words<E / 2>(out + oi, h);
+      } else {
 #pragma unroll
-      for (int hf = 0; hf < 2; ++hf) {
-        constexpr int HE = E / 2;
-        const int64_t eh = e0 + hf * HE;
-        const int cnt = (int)max((int64_t)0, min((int64_t)HE, shard_len - eh));
-        if (cnt == 0) continue;
-        uint32_t h[HE / 2];
-        uint32_t risky = (exact16 || sok) ? 0xFFFFFFFFu : 0u;
-#pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          uint32_t f[32 / BITS];
-          magic_word<BITS>(wa[2 * hf + i], f);
-#pragma unroll
-          for (int j = 0; j < 32 / BITS; j += 2) {
-            const float2 c = fadd2(make_float2(__uint_as_float(f[j]), __uint_as_float(f[j + 1])),
-                                   make_float2(-Bias<BITS>::kF, -Bias<BITS>::kF));
-            const float2 p = fmul2(c, make_float2(s32, s32));
-            if (!exact16)
-              risky = min(risky, min(Out16<O>::near_mid(__float_as_uint(p.x)), Out16<O>::near_mid(__float_as_uint(p.y))));
-            h[(i * (32 / BITS) + j) / 2] = Out16<O>::pack2(p.x, p.y);
-          }
-        }
-        if (risky == 0u) {  // rare (fp32-sourced scales only): exact f64 path for this half unit
-          const double s64 = scale_of<BITS>((double)m);
-#pragma unroll
-          for (int i = 0; i < 2; ++i) {
-            uint32_t f[32 / BITS];
-            magic_word<BITS>(wa[2 * hf + i], f);
-#pragma unroll
-            for (int j = 0; j < 32 / BITS; j += 2) {
-              O a = from_f64<O>(__dmul_rn(code_f64<BITS>(f[j]), s64));
-              O b = from_f64<O>(__dmul_rn(code_f64<BITS>(f[j + 1]), s64));
-              h[(i * (32 / BITS) + j) / 2] =
-                  (uint32_t)(*reinterpret_cast<uint16_t*>(&a)) | ((uint32_t)(*reinterpret_cast<uint16_t*>(&b)) << 16);
-            }
-          }
-        }
-        const int64_t oi = (int64_t)s * shard_len + eh;
-        O* dst = out + oi;
-        if (vec_ok && cnt == HE) {
-#pragma unroll
-          for (int i = 0; i < HE / 8; ++i)
-            reinterpret_cast<uint4*>(dst)[i] = make_uint4(h[4 * i], h[4 * i + 1], h[4 * i + 2], h[4 * i + 3]);
+        for (int i = 0; i < E; ++i)
+          if (i < cnt) store_scalar<O>(out + oi, i, h[i / 2] >> (16 * (i & 1)));
+      }
+      if (sec_out != nullptr && oi + cnt > sec_lo && oi < sec_lo + sec_len) {
+        const int64_t k0 = oi - sec_lo;
+        if (vec_ok && cnt == E && k0 >= 0 && k0 + E <= sec_len) {
+          store_words<E / 2>(sec_out + k0, h);
         } else {
 #pragma unroll
-          for (int i = 0; i < HE; ++i)
-            if (i < cnt) store_scalar<O>(dst, i, h[i / 2] >> (16 * (i & 1)));
-        }
-        if (sec_out != nullptr && oi + cnt > sec_lo && oi < sec_lo + sec_len) {
-          const int64_t k0 = oi - sec_lo;
-          if (vec_ok && cnt == HE && k0 >= 0 && k0 + HE <= sec_len) {
-#pragma unroll
-            for (int i = 0; i < HE / 8; ++i)
-              reinterpret_cast<uint4*>(sec_out + k0)[i] = make_uint4(h[4 * i], h[4 * i + 1], h[4 * i + 2], h[4 * i + 3]);
-          } else {
-#pragma unroll
-            for (int i = 0; i < HE; ++i)
-              if (i < cnt && k0 + i >= 0 && k0 + i < sec_len)
-                store_scalar<O>(sec_out + k0, i, h[i / 2] >> (16 * (i & 1)));
-          }
+          for (int i = 0; i < E; ++i)
+            if (i < cnt && k0 + i >= 0 && k0 + i < sec_len) store_scalar<O>(sec_out + k0, i, h[i / 2] >> (16 * (i & 1)));
         }
       }
     }

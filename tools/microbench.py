@@ -23,7 +23,7 @@ except Exception:
     pass
 
 
-def timeit(fn, iters=20, warm=3):
+def timeit(fn, iters=50, warm=5):
     for _ in range(warm):
         fn()
     torch.cuda.synchronize()
