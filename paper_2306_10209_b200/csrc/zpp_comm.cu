@@ -125,6 +125,7 @@ static int comm_ok(zpp_comm_t c) {
 
 static int barrier(zpp_comm_t c, int scope, int timeout_ms, uint32_t* flag, cudaStream_t st) {
   std::vector<int> m = c->members(scope);
+  if (m.size() == 1) return ZPP_OK;  // nothing to wait for
   const uint32_t e = ++c->epoch[scope];
   BarrierArgs a;
   for (size_t i = 0; i < m.size(); ++i) {

@@ -1,0 +1,285 @@
+"""ZeRO++ collectives across GPUs: one process per GPU, NVLink P2P.
+
+The single-process functions in ``collectives.py`` keep the reference's
+whole-cluster signatures (zs/collectives.py).  This module is the same three
+collectives run for real, one rank per GPU, on a symmetric device workspace
+that every rank maps through CUDA IPC:
+
+* ``Communicator.qwz_allgather``  qwZ (zs/collectives.py:244-282): K0 quantizes
+  this rank's shard into its symmetric buffer, a device barrier, then ONE
+  kernel pulls every rank's INT8 codes over NVLink and dequantizes them into
+  the local fp16 output.  Optional hpZ write-through keeps this rank's
+  secondary partition (zs/engine.py:364-367) in HBM.
+* ``Communicator.hpz_allgather``  hpZ (zs/collectives.py:202-241, groups):
+  group barrier, then a copy kernel pulls the group members' secondary shards.
+* ``Communicator.qgz_reduce_scatter``  qgZ (zs/collectives.py:464-569): per
+  stage K1 (reorder + quantize) -> group barrier -> K2 pulls the X intra-group
+  messages over NVLink and requantizes -> cross barrier -> K3 pulls the Y
+  hop-2 segments and folds them in f64.
+
+``torch.distributed`` is plumbing only: it exchanges the 64-byte IPC handles
+once and provides the NCCL comparators (``nccl_*``, the fp16/bf16 ZeRO-3
+baseline collectives and a staged qwZ/qgZ that routes the same kernels through
+NCCL all-gather / all-to-all).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import torch
+import torch.distributed as dist
+
+from . import _lib
+from .errors import ValidationError
+from .partitioner import PartitionSpec
+from .quantizer import QuantConfig, device, dtype_code, stream_ptr
+
+ALIGN = 256
+
+
+def _align(x: int) -> int:
+    return (x + ALIGN - 1) // ALIGN * ALIGN
+
+
+def members(rank: int, world: int, group_size: int, scope: str) -> list[int]:
+    """Ranks taking part in a barrier scope -- mirrors zpp_comm::members in
+    csrc/zpp_comm.cu.  world: all ranks; group: consecutive ranks of this
+    rank's group (zs/partitioner.py:67-73); cross: the ranks with this rank's
+    local index in every group (qgZ hop 2)."""
+    node, loc = divmod(rank, group_size)
+    if scope == "world":
+        return list(range(world))
+    if scope == "group":
+        return [node * group_size + j for j in range(group_size)]
+    if scope == "cross":
+        return [c * group_size + loc for c in range(world // group_size)]
+    raise ValidationError(f"unknown scope {scope!r}")
+
+
+@dataclass(frozen=True)
+class SymLayout:
+    """Byte offsets of each collective's region in the symmetric workspace."""
+
+    qwz: int
+    hpz: int
+    qgz: int
+    total: int
+
+    @staticmethod
+    def plan(qwz_bytes: int, hpz_bytes: int, qgz_bytes: int) -> "SymLayout":
+        qwz = 0
+        hpz = _align(qwz + qwz_bytes)
+        qgz = _align(hpz + hpz_bytes)
+        return SymLayout(qwz=qwz, hpz=hpz, qgz=qgz, total=_align(qgz + qgz_bytes))
+
+
+def exchange_handles(handle: bytes, group=None) -> bytes:
+    """All-gather one fixed-size blob per rank (rank order) over torch.distributed."""
+    if not (dist.is_available() and dist.is_initialized()):
+        return handle
+    out = [None] * dist.get_world_size(group)
+    dist.all_gather_object(out, handle, group=group)
+    return b"".join(out)
+
+
+class Communicator:
+    """NVLink peer-memory communicator for the fused ZeRO++ collectives.
+
+    Sizes are fixed at construction (the symmetric workspace is allocated once):
+    ``qwz_shard`` elements per rank for qwZ, ``hpz_sec`` secondary elements per
+    rank (0 = hpZ off), ``qgz_elems`` gradient elements per call for qgZ.
+    ``group_size`` is the reference's gpus_per_node (zs/topology.py:31-52); on
+    one 8xB200 box the default 2 groups x 4 GPUs stand in for 2 nodes.
+    """
+
+    def __init__(self, *, group_size: int | None = None, qwz_shard: int = 0,
+                 qwz_cfg: QuantConfig = QuantConfig(bit_width=8, block_size=2048), hpz_sec: int = 0,
+                 hpz_dtype: torch.dtype = torch.float16, qgz_elems: int = 0, qgz_stages: int = 1,
+                 qgz_cfg: QuantConfig = QuantConfig(bit_width=4, block_size=512),
+                 qgz_intra_cfg: QuantConfig | None = None):
+        self.lib = _lib.load()
+        initialized = dist.is_available() and dist.is_initialized()
+        self.rank = dist.get_rank() if initialized else 0
+        self.world = dist.get_world_size() if initialized else 1
+        if group_size is None:
+            group_size = min(self.world, 4) if self.world % min(self.world, 4) == 0 else self.world
+        if self.world % group_size:
+            raise ValidationError(f"group_size {group_size} must divide world {self.world}")
+        self.group_size = group_size
+        self.qwz_shard, self.qwz_cfg = qwz_shard, qwz_cfg
+        self.hpz_sec, self.hpz_dtype = hpz_sec, hpz_dtype
+        self.qgz_elems, self.qgz_stages = qgz_elems, qgz_stages
+        self.qgz_cfg = qgz_cfg
+        self.qgz_intra_cfg = qgz_intra_cfg or qgz_cfg
+        hpz_esz = torch.tensor([], dtype=hpz_dtype).element_size()
+        self.layout = SymLayout.plan(
+            self.lib.zpp_qwz_sym_bytes(qwz_shard, qwz_cfg.bit_width, qwz_cfg.block_size, self.world) if qwz_shard else 0,
+            self.lib.zpp_hpz_sym_bytes(hpz_sec, hpz_esz) if hpz_sec else 0,
+            self.lib.zpp_qgz_sym_bytes(qgz_elems, self.world, qgz_stages, self.qgz_intra_cfg.bit_width,
+                                       self.qgz_intra_cfg.block_size, qgz_cfg.bit_width, qgz_cfg.block_size)
+            if qgz_elems else 0)
+        device()  # fail loudly without a GPU
+        h = ctypes.c_void_p()
+        _lib.check(self.lib.zpp_comm_create(self.rank, self.world, group_size, max(self.layout.total, ALIGN),
+                                            ctypes.byref(h)), "zpp_comm_create")
+        self.handle = h
+        mine = ctypes.create_string_buffer(_lib.IPC_HANDLE_BYTES)
+        _lib.check(self.lib.zpp_comm_ipc_handle(h, mine), "zpp_comm_ipc_handle")
+        allh = exchange_handles(mine.raw)
+        buf = ctypes.create_string_buffer(allh, len(allh))
+        _lib.check(self.lib.zpp_comm_open_peers(h, buf), "zpp_comm_open_peers")
+        self.flag = torch.zeros(1, dtype=torch.int32, device=device())
+        if hpz_sec:
+            ptr = self.lib.zpp_comm_sym_ptr(h, self.rank) + self.layout.hpz
+            self._secondary = _wrap_device(ptr, hpz_sec, hpz_dtype)
+        else:
+            self._secondary = None
+        if initialized:
+            dist.barrier()
+
+    # -- collectives ---------------------------------------------------------
+
+    def qwz_allgather(self, shard: torch.Tensor, out: torch.Tensor | None = None,
+                      out_dtype: torch.dtype = torch.float16, write_secondary: bool = False) -> torch.Tensor:
+        """qwZ: every rank ends with the concatenation (rank order) of every
+        rank's dequantize(quantize(shard)) -- zs/collectives.py:244-282."""
+        n = int(shard.numel())
+        if n != self.qwz_shard:
+            raise ValidationError(f"shard has {n} elements, communicator was sized for {self.qwz_shard}")
+        if out is None:
+            out = torch.empty(n * self.world, dtype=out_dtype, device=shard.device)
+        sec_ptr, sec_lo, sec_len = None, 0, 0
+        if write_secondary:
+            if self._secondary is None:
+                raise ValidationError("communicator has no hpZ secondary region")
+            if out.dtype != self.hpz_dtype:
+                raise ValidationError("secondary partition dtype must match the gather output dtype")
+            spec = PartitionSpec(total_elems=n * self.world, world=self.world, group_size=self.group_size)
+            sec_lo, sec_hi = spec.secondary_range(self.rank)
+            if sec_hi - sec_lo != self.hpz_sec:
+                raise ValidationError("secondary shard length does not match the communicator's hpz_sec")
+            sec_len = sec_hi - sec_lo
+            sec_ptr = self._secondary.data_ptr()
+        _lib.check(self.lib.zpp_qwz_allgather(self.handle, self.layout.qwz, shard.data_ptr(), dtype_code(shard.dtype),
+                                              n, self.qwz_cfg.bit_width, self.qwz_cfg.block_size, out.data_ptr(),
+                                              dtype_code(out.dtype), sec_ptr, sec_lo, sec_len, self.flag.data_ptr(),
+                                              stream_ptr()), "qwz_allgather")
+        return out
+
+    @property
+    def secondary(self) -> torch.Tensor:
+        """This rank's hpZ secondary partition, held in the symmetric workspace."""
+        if self._secondary is None:
+            raise ValidationError("communicator has no hpZ secondary region")
+        return self._secondary
+
+    def hpz_allgather(self, out: torch.Tensor | None = None) -> torch.Tensor:
+        """hpZ: gather the group's secondary shards (member order) over NVLink."""
+        if self._secondary is None:
+            raise ValidationError("communicator has no hpZ secondary region")
+        if out is None:
+            out = torch.empty(self.hpz_sec * self.group_size, dtype=self.hpz_dtype, device=device())
+        _lib.check(self.lib.zpp_hpz_allgather(self.handle, self.layout.hpz, self.hpz_sec,
+                                              self._secondary.element_size(), out.data_ptr(), self.flag.data_ptr(),
+                                              stream_ptr()), "hpz_allgather")
+        return out
+
+    def qgz_reduce_scatter(self, grad: torch.Tensor, out: torch.Tensor | None = None,
+                           out_dtype: torch.dtype = torch.float32, reorder: bool = True) -> torch.Tensor:
+        """qgZ: this rank's partition (n/W elements) of the SUM over ranks,
+        through two codec passes -- zs/collectives.py:464-569."""
+        n = int(grad.numel())
+        if n != self.qgz_elems:
+            raise ValidationError(f"gradient has {n} elements, communicator was sized for {self.qgz_elems}")
+        if out is None:
+            out = torch.empty(n // self.world, dtype=out_dtype, device=grad.device)
+        _lib.check(self.lib.zpp_qgz_reduce_scatter(self.handle, self.layout.qgz, grad.data_ptr(),
+                                                   dtype_code(grad.dtype), n, self.qgz_stages, int(reorder),
+                                                   self.qgz_intra_cfg.bit_width, self.qgz_intra_cfg.block_size,
+                                                   self.qgz_cfg.bit_width, self.qgz_cfg.block_size, out.data_ptr(),
+                                                   dtype_code(out.dtype), self.flag.data_ptr(), stream_ptr()),
+                   "qgz_reduce_scatter")
+        return out
+
+    def barrier(self, scope: str = "world", timeout_ms: int = 60000):
+        code = {"world": 0, "group": 1, "cross": 2}[scope]
+        _lib.check(self.lib.zpp_comm_barrier(self.handle, code, timeout_ms, self.flag.data_ptr(), stream_ptr()),
+                   "barrier")
+
+    def check(self):
+        """Synchronise and raise the reference's exception for any device-side
+        condition seen since the last check (non-finite input, bad code, timeout)."""
+        v = int(self.flag.item())
+        if v:
+            self.flag.zero_()
+            _lib.raise_for_flags(v, "zpp collective")
+
+    def close(self):
+        if getattr(self, "handle", None) is not None:
+            torch.cuda.synchronize()
+            if dist.is_available() and dist.is_initialized():
+                dist.barrier()
+            self.lib.zpp_comm_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            if getattr(self, "handle", None) is not None:
+                self.lib.zpp_comm_destroy(self.handle)
+                self.handle = None
+        except Exception:
+            pass
+
+
+class _DevBuf:
+    """Minimal __cuda_array_interface__ wrapper so torch can view raw device memory."""
+
+    def __init__(self, ptr: int, n: int, dtype: torch.dtype):
+        typestr = {torch.float16: "<f2", torch.bfloat16: "<f2", torch.float32: "<f4", torch.float64: "<f8",
+                   torch.uint8: "|u1"}[dtype]
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, False), "version": 3}
+
+
+def _wrap_device(ptr: int, n: int, dtype: torch.dtype) -> torch.Tensor:
+    t = torch.as_tensor(_DevBuf(ptr, n, torch.float16 if dtype == torch.bfloat16 else dtype), device=device())
+    return t.view(torch.bfloat16) if dtype == torch.bfloat16 else t
+
+
+# ---------------------------------------------------------------------------
+# NCCL comparators (the ZeRO-3 baseline collectives and a staged ZeRO++ route)
+
+
+def nccl_allgather(shard: torch.Tensor, out: torch.Tensor | None = None, group=None) -> torch.Tensor:
+    """fp16 ZeRO-3 weight all-gather (the baseline qwZ replaces)."""
+    w = dist.get_world_size(group)
+    if out is None:
+        out = torch.empty(shard.numel() * w, dtype=shard.dtype, device=shard.device)
+    dist.all_gather_into_tensor(out, shard, group=group)
+    return out
+
+
+def nccl_reduce_scatter(grad: torch.Tensor, out: torch.Tensor | None = None, group=None) -> torch.Tensor:
+    """bf16 ZeRO-3 gradient reduce-scatter (the baseline qgZ replaces)."""
+    w = dist.get_world_size(group)
+    if out is None:
+        out = torch.empty(grad.numel() // w, dtype=grad.dtype, device=grad.device)
+    dist.reduce_scatter_tensor(out, grad, group=group)
+    return out
+
+
+def make_groups(group_size: int):
+    """(my group, my cross group) as torch.distributed process groups; every
+    rank must call this collectively."""
+    world, rank = dist.get_world_size(), dist.get_rank()
+    mine = cross = None
+    for g in range(world // group_size):
+        pg = dist.new_group(list(range(g * group_size, (g + 1) * group_size)))
+        if rank // group_size == g:
+            mine = pg
+    for loc in range(group_size):
+        pg = dist.new_group([c * group_size + loc for c in range(world // group_size)])
+        if rank % group_size == loc:
+            cross = pg
+    return mine, cross

@@ -1,0 +1,102 @@
+"""Per-rank worker for the multi-GPU parity test (launched by torchrun from
+tests/test_gpu_dist.py, one process per GPU).  Every rank regenerates all
+ranks' seeded inputs on the host, runs the fused NVLink collectives, and
+checks its own outputs bit-exactly against the CPU oracle."""
+
+import argparse
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+
+import golden_util as gu  # noqa: E402
+import paper_2306_10209_b200 as zpp  # noqa: E402
+from oracle import zpp_oracle as O  # noqa: E402
+from paper_2306_10209_b200.dist import Communicator, make_groups, nccl_allgather  # noqa: E402
+
+
+def bf16_bits(v):
+    return (np.asarray(v, np.float32).view(np.uint32) >> 16).astype(np.uint16)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--group", type=int, default=2)
+    ap.add_argument("--stages", type=int, default=2)
+    args = ap.parse_args()
+    local = int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    rank, world = dist.get_rank(), dist.get_world_size()
+    X = args.group
+    Y = world // X
+    failures = []
+
+    def check(name, ok):
+        if not ok:
+            failures.append(name)
+
+    # ---- qwZ + hpZ -----------------------------------------------------------
+    shard_len = 3 * 2048 + 1024  # ragged last block in every shard
+    total = shard_len * world
+    spec = zpp.PartitionSpec(total_elems=total, world=world, group_size=X)
+    lo, hi = spec.secondary_range(rank)
+    shards = [(np.random.default_rng(100 + r).normal(size=shard_len) * 0.02).astype(np.float16) for r in range(world)]
+    comm = Communicator(group_size=X, qwz_shard=shard_len, qwz_cfg=zpp.QuantConfig(bit_width=8, block_size=2048),
+                        hpz_sec=hi - lo, qgz_elems=args.stages * world * 1024, qgz_stages=args.stages,
+                        qgz_cfg=zpp.QuantConfig(bit_width=4, block_size=512))
+    want, _ = O.all_gather_qwz([s.astype(np.float64) for s in shards], 8, 2048)
+    want16 = want.astype(np.float16)
+    mine = torch.from_numpy(shards[rank]).cuda()
+    for it in range(3):  # exercise both halves of the double buffer
+        out = comm.qwz_allgather(mine, write_secondary=True)
+        comm.check()
+        check(f"qwz it{it}", np.array_equal(out.cpu().numpy(), want16))
+        check(f"hpz secondary it{it}", np.array_equal(comm.secondary.cpu().numpy(), want16[lo:hi]))
+        g = comm.hpz_allgather()
+        comm.check()
+        check(f"hpz gather it{it}", np.array_equal(g.cpu().numpy(), want16))
+    # f32 output of the same gather
+    out32 = comm.qwz_allgather(mine, out_dtype=torch.float32)
+    comm.check()
+    check("qwz fp32", np.array_equal(out32.cpu().numpy(), want.astype(np.float32)))
+    # NCCL comparator gathers the raw shards
+    raw = nccl_allgather(mine)
+    check("nccl allgather", np.array_equal(raw.cpu().numpy(), np.concatenate(shards)))
+
+    # ---- qgZ -----------------------------------------------------------------
+    n = args.stages * world * 1024
+    grads = [bf16_bits(np.random.default_rng(200 + r).normal(size=n) * np.exp(np.random.default_rng(300 + r).normal(size=n)) * 1e-3)
+             for r in range(world)]
+    ref = O.qgz_2hop([gu.as_f64(g, "bf16") for g in grads], X, Y, args.stages, 4, 512)[rank]
+    gt = gu.to_torch(grads[rank], "bf16")
+    for it in range(3):
+        o64 = comm.qgz_reduce_scatter(gt, out_dtype=torch.float64)
+        comm.check()
+        check(f"qgz f64 it{it}", np.array_equal(o64.cpu().numpy(), ref))
+        o32 = comm.qgz_reduce_scatter(gt)
+        comm.check()
+        check(f"qgz f32 it{it}", np.array_equal(o32.cpu().numpy(), ref.astype(np.float32)))
+    # ---- process groups for the staged comparators ---------------------------
+    mine_pg, cross_pg = make_groups(X)
+    check("groups", dist.get_world_size(mine_pg) == X and dist.get_world_size(cross_pg) == Y)
+
+    comm.close()
+    flag = torch.tensor([len(failures)], device="cuda")
+    dist.all_reduce(flag)
+    if failures:
+        print(f"rank {rank} FAILED: {failures}", flush=True)
+    elif rank == 0:
+        print(f"dist parity ok: world={world} groups={Y}x{X} stages={args.stages}", flush=True)
+    dist.destroy_process_group()
+    sys.exit(1 if int(flag.item()) else 0)
+
+
+if __name__ == "__main__":
+    main()

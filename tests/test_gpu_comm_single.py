@@ -1,0 +1,44 @@
+"""The fused-collective code path on one GPU (world = 1, no torch.distributed):
+symmetric workspace, double buffering and the three collectives, bit-exact vs
+the oracle."""
+
+import numpy as np
+import pytest
+import torch
+
+import golden_util as gu
+from oracle import zpp_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def test_world1_collectives():
+    import paper_2306_10209_b200 as zpp
+    from paper_2306_10209_b200.dist import Communicator
+
+    n = 5 * 2048 + 777
+    comm = Communicator(qwz_shard=n, hpz_sec=n, qgz_elems=4096, qgz_stages=2,
+                        qgz_cfg=zpp.QuantConfig(bit_width=4, block_size=512))
+    assert comm.world == 1 and comm.group_size == 1
+    x = (np.random.default_rng(0).normal(size=n) * 0.05).astype(np.float16)
+    want, _ = O.all_gather_qwz([x.astype(np.float64)], 8, 2048)
+    for _ in range(3):
+        out = comm.qwz_allgather(torch.from_numpy(x).cuda(), write_secondary=True)
+        comm.check()
+        assert np.array_equal(out.cpu().numpy(), want.astype(np.float16))
+        assert np.array_equal(comm.secondary.cpu().numpy(), want.astype(np.float16))
+        assert np.array_equal(comm.hpz_allgather().cpu().numpy(), want.astype(np.float16))
+    g = (np.random.default_rng(1).normal(size=4096) * 1e-3).astype(np.float32)
+    ref = O.qgz_2hop([g.astype(np.float64)], 1, 1, 2, 4, 512)[0]
+    for _ in range(3):
+        o = comm.qgz_reduce_scatter(torch.from_numpy(g).cuda(), out_dtype=torch.float64)
+        comm.check()
+        assert np.array_equal(o.cpu().numpy(), ref)
+    bad = torch.from_numpy(x).cuda()
+    bad[7] = float("nan")
+    comm.qwz_allgather(bad)
+    with pytest.raises(zpp.ValidationError):
+        comm.check()
+    with pytest.raises(zpp.ValidationError):
+        comm.qwz_allgather(torch.zeros(10, device="cuda", dtype=torch.float16))
+    comm.close()

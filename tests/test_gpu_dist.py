@@ -1,0 +1,45 @@
+"""Multi-GPU parity of the fused NVLink collectives (qwZ, hpZ, qgZ): torchrun
+one process per GPU; every rank checks its outputs bit-exactly against the
+CPU oracle (tests/dist_worker.py)."""
+
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+import torch
+
+pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _run(nproc, group, stages):
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           os.path.join(HERE, "dist_worker.py"), "--group", str(group), "--stages", str(stages)]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
+
+
+@pytest.mark.parametrize("group", [1, 2])
+def test_two_gpus(group):
+    _run(2, group, 2)
+
+
+def test_four_gpus_2x2():
+    if torch.cuda.device_count() < 4:
+        pytest.skip("needs 4 GPUs")
+    _run(4, 2, 2)
+
+
+def test_eight_gpus_2x4():
+    if torch.cuda.device_count() < 8:
+        pytest.skip("needs 8 GPUs")
+    _run(8, 4, 1)
