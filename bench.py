@@ -70,9 +70,12 @@ class ClockSampler:
     def start(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                                          "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                                          "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
+            t0 = time.time()
+            while not self.lines and time.time() - t0 < 5.0:  # first sample before the timed region
+                time.sleep(0.02)
         except Exception:
             self.proc = None
 
@@ -204,15 +207,16 @@ def run_ours(args):
 
     # ---- headline: fused qwZ all-gather -----------------------------------
     step = lambda: comm.qwz_allgather(shard, out=out)
+    clocks = ClockSampler()
+    if rank == 0:
+        clocks.start()  # sampling spans warmup + the timed region
     for _ in range(args.warmup):
         step()
     comm.check()
     barrier()
-    clocks = ClockSampler()
-    if rank == 0:
-        clocks.start()
-        time.sleep(0.3)
     t_step = timed(step, args.steps, 0)
+    if rank == 0:
+        time.sleep(0.1)
     clk = clocks.stop() if rank == 0 else None
     comm.check()
     launches_per_step = 2 + (1 if world > 1 else 0)  # quantize, [barrier], gather-dequantize

@@ -6,6 +6,7 @@
 
 #include "zpp_internal.h"
 #include "zpp_kernels.cuh"
+#include "zpp_launch.cuh"
 
 namespace zpp {
 
@@ -34,20 +35,6 @@ int sm_count() {
   });
   return cached;
 }
-
-// one resident wave of CTAs (persistent-style grid-stride), capped by work
-template <typename K>
-static int grid_for(K kernel, int threads, int64_t needed_ctas) {
-  static thread_local int dummy = 0;
-  (void)dummy;
-  int occ = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, 0) != cudaSuccess || occ <= 0) occ = 1;
-  int64_t g = (int64_t)sm_count() * occ;
-  if (needed_ctas < g) g = needed_ctas;
-  return (int)(g < 1 ? 1 : g);
-}
-
-static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 static size_t dtype_size(int dt) {
   switch (dt) {
@@ -156,20 +143,6 @@ int launch_quantize(const void* x, int dtype, const AddrSpec& a, int64_t n_out, 
 // ---------------------------------------------------------------------------
 // K4 gather-dequantize and K3 dequant-reduce
 
-static int fill_table(SrcTable& t, const void* const* codes, const void* const* absmax, int n_src) {
-  if (n_src < 1 || n_src > kMaxSrc) return fail(ZPP_ERR_VALIDATION, "n_src must be in [1, 64]");
-  for (int i = 0; i < n_src; ++i) {
-    if (!codes[i] || !absmax[i]) return fail(ZPP_ERR_VALIDATION, "null source pointer");
-    t.codes[i] = reinterpret_cast<const uint8_t*>(codes[i]);
-    t.absmax[i] = absmax[i];
-  }
-  for (int i = n_src; i < kMaxSrc; ++i) {
-    t.codes[i] = nullptr;
-    t.absmax[i] = nullptr;
-  }
-  return ZPP_OK;
-}
-
 template <int BITS, typename A, typename O>
 static int run_gather(const SrcTable& t, int n_src, int rot, int64_t shard_len, int64_t block, void* out,
                       void* sec_out, int64_t sec_lo, int64_t sec_len, uint32_t* flag, cudaStream_t st) {
@@ -180,6 +153,14 @@ static int run_gather(const SrcTable& t, int n_src, int rot, int64_t shard_len, 
     // fast 16-bit output path: one scale per 16-byte code load, aligned loads
     bool fast = block % (128 / BITS) == 0;
     for (int i = 0; i < n_src; ++i) fast = fast && aligned16(t.codes[i]);
+    if (fast && n_src > 1) {  // peers involved: latency-hiding cp.async pipeline
+      auto k = dequant16_pipe_kernel<BITS, O, 6>;
+      const int64_t tiles = ceil_div(ceil_div(shard_len, 128 / BITS), 256) * n_src;
+      const int grid = grid_for(k, 256, tiles);
+      k<<<grid, 256, 0, st>>>(t, n_src, rot, shard_len, block, reinterpret_cast<O*>(out),
+                              reinterpret_cast<O*>(sec_out), sec_lo, sec_len, vec_ok, flag);
+      return check_cuda(cudaGetLastError(), "dequant16_pipe_kernel launch");
+    }
     if (fast) {
       auto k = dequant16_kernel<BITS, O>;
       const int64_t tiles = ceil_div(ceil_div(shard_len, 128 / BITS), 32 * (BITS == 8 ? 2 : 1)) * n_src;
@@ -197,38 +178,6 @@ static int run_gather(const SrcTable& t, int n_src, int rot, int64_t shard_len, 
   return check_cuda(cudaGetLastError(), "dequant_gather_kernel launch");
 }
 
-template <int BITS, typename A, typename O>
-static int run_reduce(const SrcTable& t, int n_src, int64_t n, int64_t block, void* out, double post_scale,
-                      uint32_t* flag, cudaStream_t st) {
-  auto k = dequant_reduce_kernel<BITS, A, O>;
-  const int grid = grid_for(k, 256, ceil_div(n, 8 * 32 * 2 * 8));
-  k<<<grid, 256, 0, st>>>(t, n_src, n, block, reinterpret_cast<O*>(out), post_scale, aligned16(out), flag);
-  return check_cuda(cudaGetLastError(), "dequant_reduce_kernel launch");
-}
-
-#define ZPP_DISPATCH_BA_O(FN, ...)                                                                  \
-  do {                                                                                              \
-    if (absmax_dtype != ZPP_F32 && absmax_dtype != ZPP_F64)                                         \
-      return fail(ZPP_ERR_VALIDATION, "absmax dtype must be F32 or F64");                           \
-    const bool a64 = absmax_dtype == ZPP_F64;                                                       \
-    switch (out_dtype) {                                                                            \
-      case ZPP_F32:                                                                                 \
-        if (bits == 8) return a64 ? FN<8, double, float>(__VA_ARGS__) : FN<8, float, float>(__VA_ARGS__); \
-        return a64 ? FN<4, double, float>(__VA_ARGS__) : FN<4, float, float>(__VA_ARGS__);          \
-      case ZPP_F16:                                                                                 \
-        if (bits == 8) return a64 ? FN<8, double, __half>(__VA_ARGS__) : FN<8, float, __half>(__VA_ARGS__); \
-        return a64 ? FN<4, double, __half>(__VA_ARGS__) : FN<4, float, __half>(__VA_ARGS__);        \
-      case ZPP_BF16:                                                                                \
-        if (bits == 8)                                                                              \
-          return a64 ? FN<8, double, __nv_bfloat16>(__VA_ARGS__) : FN<8, float, __nv_bfloat16>(__VA_ARGS__); \
-        return a64 ? FN<4, double, __nv_bfloat16>(__VA_ARGS__) : FN<4, float, __nv_bfloat16>(__VA_ARGS__); \
-      case ZPP_F64:                                                                                 \
-        if (bits == 8) return a64 ? FN<8, double, double>(__VA_ARGS__) : FN<8, float, double>(__VA_ARGS__); \
-        return a64 ? FN<4, double, double>(__VA_ARGS__) : FN<4, float, double>(__VA_ARGS__);        \
-    }                                                                                               \
-    return fail(ZPP_ERR_VALIDATION, "unknown output dtype");                                        \
-  } while (0)
-
 int launch_gather_dequant(const void* const* codes, const void* const* absmax, int absmax_dtype, int n_src, int rot,
                           int64_t shard_len, int bits, int64_t block, void* out, int out_dtype, void* sec_out,
                           int64_t sec_lo, int64_t sec_len, uint32_t* flag, cudaStream_t st) {
@@ -238,86 +187,6 @@ int launch_gather_dequant(const void* const* codes, const void* const* absmax, i
   if (rc) return rc;
   rot = ((rot % n_src) + n_src) % n_src;
   ZPP_DISPATCH_BA_O(run_gather, t, n_src, rot, shard_len, block, out, sec_out, sec_lo, sec_len, flag, st);
-}
-
-int launch_dequant_reduce(const void* const* codes, const void* const* absmax, int absmax_dtype, int n_src, int64_t n,
-                          int bits, int64_t block, void* out, int out_dtype, double post_scale, uint32_t* flag,
-                          cudaStream_t st) {
-  if (n == 0) return ZPP_OK;
-  SrcTable t;
-  int rc = fill_table(t, codes, absmax, n_src);
-  if (rc) return rc;
-  ZPP_DISPATCH_BA_O(run_reduce, t, n_src, n, block, out, post_scale, flag, st);
-}
-
-// ---------------------------------------------------------------------------
-// K2
-
-bool drq_has_reg_path(int64_t out_block) {
-  return out_block == 16 || out_block == 32 || out_block == 64 || out_block == 128 || out_block == 256 ||
-         out_block == 512;
-}
-
-size_t drq_workspace_bytes(int64_t n, int64_t out_block) {
-  return (size_t)(ceil_div(n, out_block) * out_block) * sizeof(double);
-}
-
-template <int IBITS, typename IA, int OBITS, int LANES>
-static int run_drq(const SrcTable& t, int n_src, int64_t n, int64_t in_block, int64_t nbo, uint8_t* codes,
-                   double* absmax, uint32_t* flag, cudaStream_t st) {
-  auto k = drq_reg_kernel<IBITS, IA, OBITS, LANES>;
-  const int grid = grid_for(k, 256, ceil_div(nbo, 256 / LANES));
-  k<<<grid, 256, 0, st>>>(t, n_src, n, in_block, nbo, codes, absmax, flag);
-  return check_cuda(cudaGetLastError(), "drq_reg_kernel launch");
-}
-
-template <int IBITS, typename IA, int OBITS>
-static int drq_block(const SrcTable& t, int n_src, int64_t n, int64_t in_block, int64_t out_block, uint8_t* codes,
-                     double* absmax, uint32_t* flag, cudaStream_t st) {
-  const int64_t nbo = ceil_div(n, out_block);
-  switch (out_block) {
-    case 16: return run_drq<IBITS, IA, OBITS, 1>(t, n_src, n, in_block, nbo, codes, absmax, flag, st);
-    case 32: return run_drq<IBITS, IA, OBITS, 2>(t, n_src, n, in_block, nbo, codes, absmax, flag, st);
-    case 64: return run_drq<IBITS, IA, OBITS, 4>(t, n_src, n, in_block, nbo, codes, absmax, flag, st);
-    case 128: return run_drq<IBITS, IA, OBITS, 8>(t, n_src, n, in_block, nbo, codes, absmax, flag, st);
-    case 256: return run_drq<IBITS, IA, OBITS, 16>(t, n_src, n, in_block, nbo, codes, absmax, flag, st);
-    case 512: return run_drq<IBITS, IA, OBITS, 32>(t, n_src, n, in_block, nbo, codes, absmax, flag, st);
-  }
-  return fail(ZPP_ERR_VALIDATION, "no register path for this output block");
-}
-
-int launch_drq(const void* const* codes, const void* const* absmax, int absmax_dtype, int n_src, int64_t n,
-               int in_bits, int64_t in_block, int out_bits, int64_t out_block, uint8_t* out_codes,
-               double* out_absmax, void* workspace, size_t ws_bytes, uint32_t* flag, cudaStream_t st) {
-  if (n == 0) return ZPP_OK;
-  SrcTable t;
-  int rc = fill_table(t, codes, absmax, n_src);
-  if (rc) return rc;
-  if (absmax_dtype != ZPP_F32 && absmax_dtype != ZPP_F64)
-    return fail(ZPP_ERR_VALIDATION, "absmax dtype must be F32 or F64");
-  const bool a64 = absmax_dtype == ZPP_F64;
-  bool aligned = true;  // 8-element chunk loads need 8 B (INT8) / 4 B (INT4) aligned codes
-  for (int i = 0; i < n_src; ++i) aligned = aligned && (reinterpret_cast<uintptr_t>(codes[i]) % in_bits) == 0;
-  if (drq_has_reg_path(out_block) && aligned) {
-#define ZPP_DRQ(IB, OB)                                                                                  \
-  return a64 ? drq_block<IB, double, OB>(t, n_src, n, in_block, out_block, out_codes, out_absmax, flag, st) \
-             : drq_block<IB, float, OB>(t, n_src, n, in_block, out_block, out_codes, out_absmax, flag, st);
-    if (in_bits == 8 && out_bits == 8) ZPP_DRQ(8, 8)
-    if (in_bits == 8 && out_bits == 4) ZPP_DRQ(8, 4)
-    if (in_bits == 4 && out_bits == 8) ZPP_DRQ(4, 8)
-    ZPP_DRQ(4, 4)
-#undef ZPP_DRQ
-  }
-  // generic: f64 fold into the workspace (K3 with f64 output), then the
-  // generic f64 quantizer -- identical arithmetic, three launches.
-  const size_t need = drq_workspace_bytes(n, out_block);
-  if (!workspace || ws_bytes < need) return fail(ZPP_ERR_VALIDATION, "workspace too small for fused requantize");
-  rc = launch_dequant_reduce(codes, absmax, absmax_dtype, n_src, n, in_bits, in_block, workspace, ZPP_F64, 1.0, flag,
-                             st);
-  if (rc) return rc;
-  AddrSpec a;
-  a.n = n;
-  return launch_quantize(workspace, ZPP_F64, a, n, out_bits, out_block, out_codes, out_absmax, flag, st);
 }
 
 }  // namespace zpp

@@ -375,7 +375,8 @@ int zpp_qgz_reduce_scatter(zpp_comm_t c, size_t sym_offset, const void* grad, in
     }
     rc = launch_drq(codes, absmax, in_abs, X, msg_elems, intra_bits, intra_block, inter_bits, inter_block,
                     c->local + base + l.hop_codes, reinterpret_cast<double*>(c->local + base + l.hop_abs),
-                    c->local + base + l.ws, drq_workspace_bytes(msg_elems, inter_block), flag, st);
+                    c->local + base + l.ws, drq_workspace_bytes(msg_elems, inter_block), flag, st,
+                    /*validate=*/false);
     if (rc) return rc;
     rc = barrier(c, 2, kBarrierTimeoutMs, flag, st);
     if (rc) return rc;
@@ -386,7 +387,8 @@ int zpp_qgz_reduce_scatter(zpp_comm_t c, size_t sym_offset, const void* grad, in
       absmax[g] = p + l.hop_abs + (size_t)(L / inter_block) * 8 * node;
     }
     rc = launch_dequant_reduce(codes, absmax, ZPP_F64, Y, L, inter_bits, inter_block,
-                               reinterpret_cast<uint8_t*>(out) + (size_t)s * L * out_esz, out_dtype, 1.0, flag, st);
+                               reinterpret_cast<uint8_t*>(out) + (size_t)s * L * out_esz, out_dtype, 1.0, flag, st,
+                               /*validate=*/false);
     if (rc) return rc;
   }
   return ZPP_OK;

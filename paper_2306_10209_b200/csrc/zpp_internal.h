@@ -31,10 +31,11 @@ int launch_gather_dequant(const void* const* codes, const void* const* absmax, i
                           void* sec_out, int64_t sec_lo, int64_t sec_len, uint32_t* flag, cudaStream_t st);
 int launch_dequant_reduce(const void* const* codes, const void* const* absmax, int absmax_dtype, int n_src,
                           int64_t n, int bits, int64_t block, void* out, int out_dtype, double post_scale,
-                          uint32_t* flag, cudaStream_t st);
+                          uint32_t* flag, cudaStream_t st, bool validate = true);
 int launch_drq(const void* const* codes, const void* const* absmax, int absmax_dtype, int n_src, int64_t n,
                int in_bits, int64_t in_block, int out_bits, int64_t out_block, uint8_t* out_codes,
-               double* out_absmax, void* workspace, size_t ws_bytes, uint32_t* flag, cudaStream_t st);
+               double* out_absmax, void* workspace, size_t ws_bytes, uint32_t* flag, cudaStream_t st,
+               bool validate = true);
 size_t drq_workspace_bytes(int64_t n, int64_t out_block);
 bool drq_has_reg_path(int64_t out_block);
 

@@ -659,6 +659,87 @@ dequant16_kernel(SrcTable src, int n_src, int rot, int64_t shard_len, int64_t B,
 }
 
 // ---------------------------------------------------------------------------
+// K4 over NVLink: the same decode fed by a per-thread cp.async pipeline.  A
+// CTA tile is 256 units of 16 code bytes (one per thread); each thread keeps
+// PIPE-1 of its own 16-byte copies in flight in shared memory (LDGSTS works on
+// peer-mapped addresses), so the remote-read latency (~2 us over NVLink) is
+// hidden without holding registers and without any CTA-wide barrier: a thread
+// only ever reads back the bytes it copied itself.
+
+template <int BITS, typename O, int PIPE>
+__global__ void __launch_bounds__(256)
+dequant16_pipe_kernel(SrcTable src, int n_src, int rot, int64_t shard_len, int64_t B, O* __restrict__ out,
+                      O* __restrict__ sec_out, int64_t sec_lo, int64_t sec_len, int vec_ok,
+                      uint32_t* __restrict__ flag) {
+  constexpr int E = Unit16B<BITS>::E;
+  __shared__ uint4 ring[PIPE][256];
+  const int tid = threadIdx.x;
+  const int units = (int)((shard_len + E - 1) / E);
+  const int tiles = (units + 255) / 256;
+  const int n_tiles = tiles * n_src;
+  const bool pow2 = (B & (B - 1)) == 0;
+  const int lg = pow2 ? __ffsll(B) - 1 : 0;
+  bool bad = false;
+  // tile k of this CTA: g = blockIdx.x + k * gridDim.x
+  auto src_of = [&](int g, int& s, int& unit) {
+    const int t = g / n_src;
+    s = g - t * n_src + rot;
+    if (s >= n_src) s -= n_src;
+    unit = t * 256 + tid;
+  };
+  auto issue = [&](int g, int slot) {
+    if (g < n_tiles) {
+      int s, unit;
+      src_of(g, s, unit);
+      if (unit < units) {
+        const uint4* gp = reinterpret_cast<const uint4*>(src.codes[s]) + unit;
+        const uint32_t sp = (uint32_t)__cvta_generic_to_shared(&ring[slot][tid]);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sp), "l"(gp) : "memory");
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  int g = blockIdx.x;
+#pragma unroll
+  for (int k = 0; k < PIPE - 1; ++k) issue(g + k * (int)gridDim.x, k);
+  for (int k = 0; g < n_tiles; ++k, g += gridDim.x) {
+    asm volatile("cp.async.wait_group %0;" ::"n"(PIPE - 2) : "memory");
+    const int slot = k % PIPE;
+    const uint4 w = ring[slot][tid];
+    issue(g + (PIPE - 1) * (int)gridDim.x, (k + PIPE - 1) % PIPE);
+    int s, unit;
+    src_of(g, s, unit);
+    if (unit >= units) continue;
+    bad |= bad_codes(w, BITS);
+    const int64_t e0 = (int64_t)unit * E;
+    const float m = __ldg(reinterpret_cast<const float*>(src.absmax[s]) + (pow2 ? (e0 >> lg) : e0 / B));
+    uint32_t h[E / 2];
+    decode16_any<BITS, O>(w, m, h);
+    const int cnt = (int)min((int64_t)E, shard_len - e0);
+    const int64_t oi = (int64_t)s * shard_len + e0;
+    if (vec_ok && cnt == E) {
+      store_words<E / 2>(out + oi, h);
+    } else {
+#pragma unroll
+      for (int i = 0; i < E; ++i)
+        if (i < cnt) store_scalar<O>(out + oi, i, h[i / 2] >> (16 * (i & 1)));
+    }
+    if (sec_out != nullptr && oi + cnt > sec_lo && oi < sec_lo + sec_len) {
+      const int64_t k0 = oi - sec_lo;
+      if (vec_ok && cnt == E && k0 >= 0 && k0 + E <= sec_len) {
+        store_words<E / 2>(sec_out + k0, h);
+      } else {
+#pragma unroll
+        for (int i = 0; i < E; ++i)
+          if (i < cnt && k0 + i >= 0 && k0 + i < sec_len) store_scalar<O>(sec_out + k0, i, h[i / 2] >> (16 * (i & 1)));
+      }
+    }
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  if (bad) raise_flag(flag, FLAG_BADCODE);
+}
+
+// ---------------------------------------------------------------------------
 // exact (f64) decode of 8-element chunks, for fp32/f64 outputs, f64 absmax,
 // odd block sizes and odd alignments
 
@@ -928,6 +1009,193 @@ drq_reg_kernel(SrcTable src, int n_src, int64_t n, int64_t B1, int64_t n_blocks_
       } else {
         *reinterpret_cast<uint2*>(dst) = make_uint2(pack8_int4(q0), pack8_int4(q1));
       }
+    }
+  }
+  if (bad) raise_flag(flag, FLAG_BADCODE);
+}
+
+// ---------------------------------------------------------------------------
+// 16-element lanes for the f64 reduce kernels (K2 fast path, K3 fast path):
+// one load of 16 codes per source (INT8: 16 B, INT4: 8 B), one block scale per
+// source (host guarantees block % 16 == 0 and aligned code pointers).
+
+template <int BITS> struct Vec16;
+template <> struct Vec16<8> { using T = uint4; };
+template <> struct Vec16<4> { using T = uint2; };
+
+// acc[i] = RN64(acc[i] + RN64(code_i * s)) for the 16 codes in w -- the
+// reference's fold step (zs/quantizer.py:255-257, zs/collectives.py:71-75).
+// Each code becomes an exact double as 2^52+2^51+(code+bias) - (2^52+2^51+bias):
+// one PRMT builds the low word, one DADD removes the bias.
+template <int BITS, bool VALIDATE>
+__device__ __forceinline__ void fold16(const typename Vec16<BITS>::T& w, double s, double (&acc)[16], bool& bad) {
+  const uint32_t* ww = reinterpret_cast<const uint32_t*>(&w);
+  if constexpr (BITS == 8) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if constexpr (VALIDATE) bad |= has_byte_0x80(ww[k]);
+      const uint32_t b = ww[k] ^ 0x80808080u;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const double c = __dsub_rn(__hiloint2double(0x43380000, (int)__byte_perm(b, 0, 0x4440 + j)), Bias<8>::kD);
+        acc[4 * k + j] = __dadd_rn(acc[4 * k + j], __dmul_rn(c, s));
+      }
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      if constexpr (VALIDATE) bad |= has_nibble_8(ww[k]);
+      const uint32_t b = ww[k] ^ 0x88888888u;
+      const uint32_t ev = b & 0x0F0F0F0Fu, od = (b >> 4) & 0x0F0F0F0Fu;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const double c0 = __dsub_rn(__hiloint2double(0x43380000, (int)__byte_perm(ev, 0, 0x4440 + j)), Bias<4>::kD);
+        const double c1 = __dsub_rn(__hiloint2double(0x43380000, (int)__byte_perm(od, 0, 0x4440 + j)), Bias<4>::kD);
+        acc[8 * k + 2 * j] = __dadd_rn(acc[8 * k + 2 * j], __dmul_rn(c0, s));
+        acc[8 * k + 2 * j + 1] = __dadd_rn(acc[8 * k + 2 * j + 1], __dmul_rn(c1, s));
+      }
+    }
+  }
+}
+
+// K3 fast path: lane = 16 contiguous elements, loads of up to 4 sources in
+// flight, f64 fold in source order from +0.0, one rounding to the output type.
+template <int BITS, typename A, typename O, bool VALIDATE>
+__global__ void __launch_bounds__(256)
+dequant_reduce16_kernel(SrcTable src, int n_src, int64_t n, int64_t B, O* __restrict__ out, double post_scale,
+                        uint32_t* __restrict__ flag) {
+  using V = typename Vec16<BITS>::T;
+  constexpr int SB = 4;
+  const int64_t units = n / 16;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const bool pow2 = (B & (B - 1)) == 0;
+  const int lg = pow2 ? __ffsll(B) - 1 : 0;
+  bool bad = false;
+  for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < units; u += stride) {
+    const int64_t e0 = u * 16;
+    const int64_t blk = pow2 ? (e0 >> lg) : e0 / B;
+    double acc[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) acc[i] = 0.0;
+    for (int s0 = 0; s0 < n_src; s0 += SB) {
+      V w[SB];
+      double sc[SB];
+#pragma unroll
+      for (int j = 0; j < SB; ++j) {
+        if (s0 + j < n_src) {
+          w[j] = __ldg(reinterpret_cast<const V*>(src.codes[s0 + j]) + u);
+          sc[j] = absmax_f64<A>(reinterpret_cast<const A*>(src.absmax[s0 + j]), blk);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < SB; ++j) {
+        if (s0 + j >= n_src) break;
+        fold16<BITS, VALIDATE>(w[j], scale_of<BITS>(sc[j]), acc, bad);
+      }
+    }
+    if (post_scale != 1.0) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) acc[i] = __dmul_rn(acc[i], post_scale);
+    }
+    O* dst = out + e0;
+    if constexpr (sizeof(O) == 4) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        reinterpret_cast<float4*>(dst)[i] = make_float4(from_f64<float>(acc[4 * i]), from_f64<float>(acc[4 * i + 1]),
+                                                        from_f64<float>(acc[4 * i + 2]), from_f64<float>(acc[4 * i + 3]));
+    } else if constexpr (sizeof(O) == 8) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) reinterpret_cast<double2*>(dst)[i] = make_double2(acc[2 * i], acc[2 * i + 1]);
+    } else {
+      uint32_t h[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        O a = from_f64<O>(acc[2 * i]), b = from_f64<O>(acc[2 * i + 1]);
+        h[i] = (uint32_t)(*reinterpret_cast<uint16_t*>(&a)) | ((uint32_t)(*reinterpret_cast<uint16_t*>(&b)) << 16);
+      }
+      store_words<8>(dst, h);
+    }
+  }
+  if (bad) raise_flag(flag, FLAG_BADCODE);
+}
+
+// K2 fast path: a team of LANES lanes owns one output block of B2 = 16*LANES
+// elements, lane = 16 contiguous elements; sources folded in order (loads of
+// up to 4 in flight); requantized from the exact f64 block absmax (stored in
+// f64).  Requires n % 16 == 0, input block % 16 == 0, aligned code pointers.
+template <int IBITS, typename IA, int OBITS, int LANES, bool VALIDATE>
+__global__ void __launch_bounds__(256)
+drq16_kernel(SrcTable src, int n_src, int64_t n, int64_t B1, int64_t n_blocks_out, uint8_t* __restrict__ codes,
+             double* __restrict__ absmax, uint32_t* __restrict__ flag) {
+  using V = typename Vec16<IBITS>::T;
+  constexpr int B2 = LANES * 16;
+  constexpr int TPW = 32 / LANES;
+  constexpr int QMAX = Codes<OBITS>::kQmax;
+  constexpr int SB = 4;
+  const int lane = threadIdx.x & 31;
+  const int tl = lane % LANES;
+  const int team = lane / LANES;
+  const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarp = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const bool pow2 = (B1 & (B1 - 1)) == 0;
+  const int lg = pow2 ? __ffsll(B1) - 1 : 0;
+  bool bad = false;
+  for (int64_t wb = gwarp * TPW; wb < n_blocks_out; wb += nwarp * TPW) {
+    const int64_t b = wb + team;
+    const int64_t e0 = b * B2 + (int64_t)tl * 16;
+    const bool active = b < n_blocks_out && e0 < n;  // n % 16 == 0: lanes are all-valid or all-empty
+    const int64_t u = e0 / 16;
+    const int64_t ib = pow2 ? (e0 >> lg) : e0 / B1;
+    double acc[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) acc[i] = 0.0;
+    for (int s0 = 0; s0 < n_src; s0 += SB) {
+      V w[SB];
+      double sc[SB];
+#pragma unroll
+      for (int j = 0; j < SB; ++j) {
+        if (active && s0 + j < n_src) {
+          w[j] = __ldg(reinterpret_cast<const V*>(src.codes[s0 + j]) + u);
+          sc[j] = absmax_f64<IA>(reinterpret_cast<const IA*>(src.absmax[s0 + j]), ib);
+        }
+      }
+      if (active) {
+#pragma unroll
+        for (int j = 0; j < SB; ++j) {
+          if (s0 + j >= n_src) break;
+          fold16<IBITS, VALIDATE>(w[j], scale_of<IBITS>(sc[j]), acc, bad);
+        }
+      }
+    }
+    double mx = 0.0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) mx = fmax(mx, fabs(acc[i]));
+#pragma unroll
+    for (int off = LANES / 2; off >= 1; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+    if (b < n_blocks_out && tl == 0) {
+      absmax[b] = mx;
+      if (!(mx <= DBL_MAX)) raise_flag(flag, FLAG_NONFINITE);
+    }
+    if (active) {
+      const double inv = mx > 0.0 ? __ddiv_rn((double)QMAX, mx) : 0.0;
+      uint32_t q0[8], q1[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {  // |acc*inv| <= qmax: no clamp needed
+        q0[i] = (uint32_t)rint_f64(__dmul_rn(acc[i], inv));
+        q1[i] = (uint32_t)rint_f64(__dmul_rn(acc[8 + i], inv));
+      }
+      uint8_t* dst = codes + u * 2 * OBITS;
+      if constexpr (OBITS == 8) {
+        const uint2 a = pack8_int8(q0), c = pack8_int8(q1);
+        *reinterpret_cast<uint4*>(dst) = make_uint4(a.x, a.y, c.x, c.y);
+      } else {
+        *reinterpret_cast<uint2*>(dst) = make_uint2(pack8_int4(q0), pack8_int4(q1));
+      }
+    } else if (b < n_blocks_out) {
+      // zero padding of a partial last block (zs/quantizer.py:215-217)
+      uint8_t* dst = codes + u * 2 * OBITS;
+      if constexpr (OBITS == 8) *reinterpret_cast<uint4*>(dst) = make_uint4(0, 0, 0, 0);
+      else *reinterpret_cast<uint2*>(dst) = make_uint2(0, 0);
     }
   }
   if (bad) raise_flag(flag, FLAG_BADCODE);

@@ -1,0 +1,61 @@
+// Launch helpers shared by the host translation units.
+#pragma once
+
+#include "zpp_internal.h"
+#include "zpp_kernels.cuh"
+
+namespace zpp {
+
+// one resident wave of CTAs (persistent-style grid-stride), capped by work
+template <typename K>
+inline int grid_for(K kernel, int threads, int64_t needed_ctas) {
+  static thread_local int dummy = 0;
+  (void)dummy;
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, 0) != cudaSuccess || occ <= 0) occ = 1;
+  int64_t g = (int64_t)sm_count() * occ;
+  if (needed_ctas < g) g = needed_ctas;
+  return (int)(g < 1 ? 1 : g);
+}
+
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+inline int fill_table(SrcTable& t, const void* const* codes, const void* const* absmax, int n_src) {
+  if (n_src < 1 || n_src > kMaxSrc) return fail(ZPP_ERR_VALIDATION, "n_src must be in [1, 64]");
+  for (int i = 0; i < n_src; ++i) {
+    if (!codes[i] || !absmax[i]) return fail(ZPP_ERR_VALIDATION, "null source pointer");
+    t.codes[i] = reinterpret_cast<const uint8_t*>(codes[i]);
+    t.absmax[i] = absmax[i];
+  }
+  for (int i = n_src; i < kMaxSrc; ++i) {
+    t.codes[i] = nullptr;
+    t.absmax[i] = nullptr;
+  }
+  return ZPP_OK;
+}
+
+}  // namespace zpp
+
+#define ZPP_DISPATCH_BA_O(FN, ...)                                                                  \
+  do {                                                                                              \
+    if (absmax_dtype != ZPP_F32 && absmax_dtype != ZPP_F64)                                         \
+      return fail(ZPP_ERR_VALIDATION, "absmax dtype must be F32 or F64");                           \
+    const bool a64 = absmax_dtype == ZPP_F64;                                                       \
+    switch (out_dtype) {                                                                            \
+      case ZPP_F32:                                                                                 \
+        if (bits == 8) return a64 ? FN<8, double, float>(__VA_ARGS__) : FN<8, float, float>(__VA_ARGS__); \
+        return a64 ? FN<4, double, float>(__VA_ARGS__) : FN<4, float, float>(__VA_ARGS__);          \
+      case ZPP_F16:                                                                                 \
+        if (bits == 8) return a64 ? FN<8, double, __half>(__VA_ARGS__) : FN<8, float, __half>(__VA_ARGS__); \
+        return a64 ? FN<4, double, __half>(__VA_ARGS__) : FN<4, float, __half>(__VA_ARGS__);        \
+      case ZPP_BF16:                                                                                \
+        if (bits == 8)                                                                              \
+          return a64 ? FN<8, double, __nv_bfloat16>(__VA_ARGS__) : FN<8, float, __nv_bfloat16>(__VA_ARGS__); \
+        return a64 ? FN<4, double, __nv_bfloat16>(__VA_ARGS__) : FN<4, float, __nv_bfloat16>(__VA_ARGS__); \
+      case ZPP_F64:                                                                                 \
+        if (bits == 8) return a64 ? FN<8, double, double>(__VA_ARGS__) : FN<8, float, double>(__VA_ARGS__); \
+        return a64 ? FN<4, double, double>(__VA_ARGS__) : FN<4, float, double>(__VA_ARGS__);        \
+    }                                                                                               \
+    return fail(ZPP_ERR_VALIDATION, "unknown output dtype");                                        \
+  } while (0)
+

@@ -1,0 +1,129 @@
+// Host launchers for the f64 reduce kernels: K3 (dequant -> reduce,
+// BlockCodec.reduce_final, zs/collectives.py:71-75) and K2 (dequant -> reduce
+// -> requant, fused_dequant_reduce_quant, zs/quantizer.py:241-258).  Each has a
+// 16-element fast path (block % 16 == 0, n % 16 == 0, aligned codes) and the
+// general 8-element kernels for odd block sizes and alignments.  `validate`
+// turns the IntegrityError code check on (API calls) or off (internal qgZ hops,
+// whose codes come from this library's own quantizer).
+#include "zpp_internal.h"
+#include "zpp_kernels.cuh"
+#include "zpp_launch.cuh"
+
+namespace zpp {
+
+static bool codes_aligned(const SrcTable& t, int n_src, int bits) {
+  for (int i = 0; i < n_src; ++i)
+    if ((reinterpret_cast<uintptr_t>(t.codes[i]) % (2 * bits)) != 0) return false;
+  return true;
+}
+
+// ---------------------------------------------------------------------------
+// K3
+
+template <int BITS, typename A, typename O>
+static int run_reduce(const SrcTable& t, int n_src, int64_t n, int64_t block, void* out, double post_scale,
+                      bool validate, uint32_t* flag, cudaStream_t st) {
+  if (n % 16 == 0 && block % 16 == 0 && aligned16(out) && codes_aligned(t, n_src, BITS)) {
+    auto k = validate ? dequant_reduce16_kernel<BITS, A, O, true> : dequant_reduce16_kernel<BITS, A, O, false>;
+    const int grid = grid_for(k, 256, ceil_div(n / 16, 256));
+    k<<<grid, 256, 0, st>>>(t, n_src, n, block, reinterpret_cast<O*>(out), post_scale, flag);
+    return check_cuda(cudaGetLastError(), "dequant_reduce16_kernel launch");
+  }
+  auto k = dequant_reduce_kernel<BITS, A, O>;
+  const int grid = grid_for(k, 256, ceil_div(n, 8 * 32 * 2 * 8));
+  k<<<grid, 256, 0, st>>>(t, n_src, n, block, reinterpret_cast<O*>(out), post_scale, aligned16(out), flag);
+  return check_cuda(cudaGetLastError(), "dequant_reduce_kernel launch");
+}
+
+int launch_dequant_reduce(const void* const* codes, const void* const* absmax, int absmax_dtype, int n_src, int64_t n,
+                          int bits, int64_t block, void* out, int out_dtype, double post_scale, uint32_t* flag,
+                          cudaStream_t st, bool validate) {
+  if (n == 0) return ZPP_OK;
+  SrcTable t;
+  int rc = fill_table(t, codes, absmax, n_src);
+  if (rc) return rc;
+  ZPP_DISPATCH_BA_O(run_reduce, t, n_src, n, block, out, post_scale, validate, flag, st);
+}
+
+// ---------------------------------------------------------------------------
+// K2
+
+bool drq_has_reg_path(int64_t out_block) {
+  return out_block == 16 || out_block == 32 || out_block == 64 || out_block == 128 || out_block == 256 ||
+         out_block == 512;
+}
+
+size_t drq_workspace_bytes(int64_t n, int64_t out_block) {
+  return (size_t)(ceil_div(n, out_block) * out_block) * sizeof(double);
+}
+
+template <int IBITS, typename IA, int OBITS, int LANES>
+static int run_drq(const SrcTable& t, int n_src, int64_t n, int64_t in_block, int64_t nbo, uint8_t* codes,
+                   double* absmax, bool validate, uint32_t* flag, cudaStream_t st) {
+  if (n % 16 == 0 && in_block % 16 == 0 && codes_aligned(t, n_src, IBITS)) {
+    auto k = validate ? drq16_kernel<IBITS, IA, OBITS, LANES, true> : drq16_kernel<IBITS, IA, OBITS, LANES, false>;
+    const int grid = grid_for(k, 256, ceil_div(nbo, 256 / LANES));
+    k<<<grid, 256, 0, st>>>(t, n_src, n, in_block, nbo, codes, absmax, flag);
+    return check_cuda(cudaGetLastError(), "drq16_kernel launch");
+  }
+  auto k = drq_reg_kernel<IBITS, IA, OBITS, LANES>;
+  const int grid = grid_for(k, 256, ceil_div(nbo, 256 / LANES));
+  k<<<grid, 256, 0, st>>>(t, n_src, n, in_block, nbo, codes, absmax, flag);
+  return check_cuda(cudaGetLastError(), "drq_reg_kernel launch");
+}
+
+template <int IBITS, typename IA, int OBITS>
+static int drq_block(const SrcTable& t, int n_src, int64_t n, int64_t in_block, int64_t out_block, uint8_t* codes,
+                     double* absmax, bool validate, uint32_t* flag, cudaStream_t st) {
+  const int64_t nbo = ceil_div(n, out_block);
+#define ZPP_RUN(L) return run_drq<IBITS, IA, OBITS, L>(t, n_src, n, in_block, nbo, codes, absmax, validate, flag, st)
+  switch (out_block) {
+    case 16: ZPP_RUN(1);
+    case 32: ZPP_RUN(2);
+    case 64: ZPP_RUN(4);
+    case 128: ZPP_RUN(8);
+    case 256: ZPP_RUN(16);
+    case 512: ZPP_RUN(32);
+  }
+#undef ZPP_RUN
+  return fail(ZPP_ERR_VALIDATION, "no register path for this output block");
+}
+
+int launch_drq(const void* const* codes, const void* const* absmax, int absmax_dtype, int n_src, int64_t n,
+               int in_bits, int64_t in_block, int out_bits, int64_t out_block, uint8_t* out_codes,
+               double* out_absmax, void* workspace, size_t ws_bytes, uint32_t* flag, cudaStream_t st,
+               bool validate) {
+  if (n == 0) return ZPP_OK;
+  SrcTable t;
+  int rc = fill_table(t, codes, absmax, n_src);
+  if (rc) return rc;
+  if (absmax_dtype != ZPP_F32 && absmax_dtype != ZPP_F64)
+    return fail(ZPP_ERR_VALIDATION, "absmax dtype must be F32 or F64");
+  const bool a64 = absmax_dtype == ZPP_F64;
+  bool aligned = true;  // 8-element chunk loads need 8 B (INT8) / 4 B (INT4) aligned codes
+  for (int i = 0; i < n_src; ++i) aligned = aligned && (reinterpret_cast<uintptr_t>(codes[i]) % in_bits) == 0;
+  if (drq_has_reg_path(out_block) && aligned) {
+#define ZPP_DRQ(IB, OB)                                                                                        \
+  return a64 ? drq_block<IB, double, OB>(t, n_src, n, in_block, out_block, out_codes, out_absmax, validate,  \
+                                         flag, st)                                                           \
+             : drq_block<IB, float, OB>(t, n_src, n, in_block, out_block, out_codes, out_absmax, validate,   \
+                                        flag, st);
+    if (in_bits == 8 && out_bits == 8) ZPP_DRQ(8, 8)
+    if (in_bits == 8 && out_bits == 4) ZPP_DRQ(8, 4)
+    if (in_bits == 4 && out_bits == 8) ZPP_DRQ(4, 8)
+    ZPP_DRQ(4, 4)
+#undef ZPP_DRQ
+  }
+  // generic: f64 fold into the workspace (K3 with f64 output), then the
+  // generic f64 quantizer -- identical arithmetic, three launches.
+  const size_t need = drq_workspace_bytes(n, out_block);
+  if (!workspace || ws_bytes < need) return fail(ZPP_ERR_VALIDATION, "workspace too small for fused requantize");
+  rc = launch_dequant_reduce(codes, absmax, absmax_dtype, n_src, n, in_bits, in_block, workspace, ZPP_F64, 1.0, flag,
+                             st, validate);
+  if (rc) return rc;
+  AddrSpec a;
+  a.n = n;
+  return launch_quantize(workspace, ZPP_F64, a, n, out_bits, out_block, out_codes, out_absmax, flag, st);
+}
+
+}  // namespace zpp
