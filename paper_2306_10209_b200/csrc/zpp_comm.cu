@@ -97,6 +97,10 @@ struct zpp_comm {
   uint64_t qwz_uses = 0, qgz_uses = 0;
   cudaIpcMemHandle_t handle;
   int device = 0;
+  // qgZ stage pipelining: K1 of stage s+1 runs on `side` while K2/K3 of stage
+  // s run on the caller's stream
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_k1 = nullptr, ev_bar = nullptr;
 
   uint32_t* flag_slot(int owner, int scope, int writer) {
     return reinterpret_cast<uint32_t*>(peers[owner] + sym_bytes) + scope * kMaxRanks + writer;
@@ -210,6 +214,12 @@ int zpp_comm_barrier(zpp_comm_t c, int scope, int timeout_ms, void* errflag, voi
 int zpp_comm_destroy(zpp_comm_t c) {
   if (!c) return ZPP_OK;
   cudaDeviceSynchronize();
+  if (c->side) {
+    cudaEventDestroy(c->ev_start);
+    cudaEventDestroy(c->ev_k1);
+    cudaEventDestroy(c->ev_bar);
+    cudaStreamDestroy(c->side);
+  }
   for (int r = 0; r < c->world; ++r)
     if (c->opened[r]) cudaIpcCloseMemHandle(c->peers[r]);
   cudaFree(c->local);
@@ -349,9 +359,19 @@ int zpp_qgz_reduce_scatter(zpp_comm_t c, size_t sym_offset, const void* grad, in
   const size_t out_esz = out_dtype == ZPP_F64 ? 8 : (out_dtype == ZPP_F32 ? 4 : 2);
   const int64_t L = l.L;
   const int64_t msg_elems = (int64_t)Y * L;  // one hop-1 message
-  for (int s = 0; s < stages; ++s) {
-    const size_t base = sym_offset + (c->qgz_uses++ & 1) * l.region;
-    // K1: swizzle + quantize this stage's slices into my send buffer [j][c][e]
+  const bool pipelined = stages > 1;
+  if (pipelined && !c->side) {
+    rc = check_cuda(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking), "side stream");
+    if (!rc) rc = check_cuda(cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming), "event");
+    if (!rc) rc = check_cuda(cudaEventCreateWithFlags(&c->ev_k1, cudaEventDisableTiming), "event");
+    if (!rc) rc = check_cuda(cudaEventCreateWithFlags(&c->ev_bar, cudaEventDisableTiming), "event");
+    if (rc) return rc;
+  }
+  const uint64_t use0 = c->qgz_uses;
+  c->qgz_uses += stages;
+  auto base_of = [&](int s) { return sym_offset + ((use0 + s) & 1) * l.region; };
+  // K1: swizzle + quantize stage s's slices into my send buffer [j][c][e]
+  auto k1 = [&](int s, cudaStream_t on) {
     AddrSpec a;
     a.swizzle = true;
     a.L = L;
@@ -360,11 +380,34 @@ int zpp_qgz_reduce_scatter(zpp_comm_t c, size_t sym_offset, const void* grad, in
     a.X = X;
     a.Y = Y;
     a.reorder = reorder ? 1 : 0;
-    rc = launch_quantize(grad, dtype, a, (int64_t)W * L, intra_bits, intra_block, c->local + base + l.send_codes,
-                         c->local + base + l.send_abs, flag, st);
-    if (rc) return rc;
+    const size_t base = base_of(s);
+    return launch_quantize(grad, dtype, a, (int64_t)W * L, intra_bits, intra_block, c->local + base + l.send_codes,
+                           c->local + base + l.send_abs, flag, on);
+  };
+  if (pipelined) {
+    // K1(s) rewrites the send half used by stage s-2, whose readers (group
+    // peers' K2(s-2)) all finished before they reached group barrier(s-1);
+    // so K1(s) only waits for that barrier, and overlaps K2/K3(s-1).
+    if ((rc = check_cuda(cudaEventRecord(c->ev_start, st), "record"))) return rc;
+    if ((rc = check_cuda(cudaStreamWaitEvent(c->side, c->ev_start, 0), "wait"))) return rc;
+    if ((rc = k1(0, c->side))) return rc;
+    if ((rc = check_cuda(cudaEventRecord(c->ev_k1, c->side), "record"))) return rc;
+  }
+  for (int s = 0; s < stages; ++s) {
+    const size_t base = base_of(s);
+    if (pipelined) {
+      if ((rc = check_cuda(cudaStreamWaitEvent(st, c->ev_k1, 0), "wait"))) return rc;
+    } else if ((rc = k1(s, st))) {
+      return rc;
+    }
     rc = barrier(c, 1, kBarrierTimeoutMs, flag, st);
     if (rc) return rc;
+    if (pipelined && s + 1 < stages) {
+      if ((rc = check_cuda(cudaEventRecord(c->ev_bar, st), "record"))) return rc;
+      if ((rc = check_cuda(cudaStreamWaitEvent(c->side, c->ev_bar, 0), "wait"))) return rc;
+      if ((rc = k1(s + 1, c->side))) return rc;
+      if ((rc = check_cuda(cudaEventRecord(c->ev_k1, c->side), "record"))) return rc;
+    }
     // K2: pull message `loc` from every group member (ascending local rank)
     const void* codes[kMaxRanks];
     const void* absmax[kMaxRanks];

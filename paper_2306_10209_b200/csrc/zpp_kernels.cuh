@@ -667,7 +667,7 @@ dequant16_kernel(SrcTable src, int n_src, int rot, int64_t shard_len, int64_t B,
 // only ever reads back the bytes it copied itself.
 
 template <int BITS, typename O, int PIPE>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 4)
 dequant16_pipe_kernel(SrcTable src, int n_src, int rot, int64_t shard_len, int64_t B, O* __restrict__ out,
                       O* __restrict__ sec_out, int64_t sec_lo, int64_t sec_len, int vec_ok,
                       uint32_t* __restrict__ flag) {
@@ -736,6 +736,123 @@ dequant16_pipe_kernel(SrcTable src, int n_src, int rot, int64_t shard_len, int64
     }
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
+  if (bad) raise_flag(flag, FLAG_BADCODE);
+}
+
+// ---------------------------------------------------------------------------
+// K4 over NVLink, TMA variant: one elected thread streams TILE-byte tiles of
+// codes from the (peer) source with cp.async.bulk into a STAGES-deep shared
+// ring, completion tracked by mbarrier transaction counts; all 256 threads
+// decode from shared memory.  Large bulk requests cut per-request overhead on
+// the NVLink read path.
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(smem)),
+               "l"(gmem), "r"(bytes), "r"((uint32_t)__cvta_generic_to_shared(bar))
+               : "memory");
+}
+
+template <int BITS, typename O, int STAGES, int TILE_U>
+__global__ void __launch_bounds__(256)
+dequant16_tma_kernel(SrcTable src, int n_src, int rot, int64_t shard_len, int64_t B, O* __restrict__ out,
+                     O* __restrict__ sec_out, int64_t sec_lo, int64_t sec_len, int vec_ok,
+                     uint32_t* __restrict__ flag) {
+  constexpr int E = Unit16B<BITS>::E;
+  constexpr int UPT = TILE_U / 256;  // units per thread per tile
+  extern __shared__ __align__(128) uint8_t dsm[];  // [STAGES][TILE_U] uint4 ring, then STAGES mbarriers
+  uint4 (*ring)[TILE_U] = reinterpret_cast<uint4 (*)[TILE_U]>(dsm);
+  uint64_t* full = reinterpret_cast<uint64_t*>(dsm + (size_t)STAGES * TILE_U * 16);
+  const int tid = threadIdx.x;
+  const int units = (int)((shard_len + E - 1) / E);
+  const int tiles = (units + TILE_U - 1) / TILE_U;
+  const int n_tiles = tiles * n_src;
+  const bool pow2 = (B & (B - 1)) == 0;
+  const int lg = pow2 ? __ffsll(B) - 1 : 0;
+  if (tid == 0) {
+#pragma unroll
+    for (int i = 0; i < STAGES; ++i) mbar_init(&full[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto locate = [&](int g, int& s, int& t) {
+    t = g / n_src;
+    s = g - t * n_src + rot;
+    if (s >= n_src) s -= n_src;
+  };
+  auto issue = [&](int g, int slot) {  // thread 0 only
+    if (g < n_tiles) {
+      int s, t;
+      locate(g, s, t);
+      const int u0 = t * TILE_U;
+      const uint32_t bytes = (uint32_t)min(TILE_U, units - u0) * 16u;
+      mbar_expect_tx(&full[slot], bytes);
+      bulk_g2s(&ring[slot][0], reinterpret_cast<const uint4*>(src.codes[s]) + u0, bytes, &full[slot]);
+    }
+  };
+  const int G = gridDim.x;
+  if (tid == 0) {
+#pragma unroll
+    for (int k = 0; k < STAGES - 1; ++k) issue(blockIdx.x + k * G, k);
+  }
+  bool bad = false;
+  int k = 0;
+  for (int g = blockIdx.x; g < n_tiles; g += G, ++k) {
+    const int slot = k % STAGES;
+    if (tid == 0) issue(g + (STAGES - 1) * G, (k + STAGES - 1) % STAGES);
+    mbar_wait(&full[slot], (uint32_t)((k / STAGES) & 1));
+    int s, t;
+    locate(g, s, t);
+    const float* am = reinterpret_cast<const float*>(src.absmax[s]);
+#pragma unroll
+    for (int j = 0; j < UPT; ++j) {
+      const int lu = j * 256 + tid;
+      const int unit = t * TILE_U + lu;
+      if (unit >= units) continue;
+      const uint4 w = ring[slot][lu];
+      bad |= bad_codes(w, BITS);
+      const int64_t e0 = (int64_t)unit * E;
+      const float m = __ldg(am + (pow2 ? (e0 >> lg) : e0 / B));
+      uint32_t h[E / 2];
+      decode16_any<BITS, O>(w, m, h);
+      const int cnt = (int)min((int64_t)E, shard_len - e0);
+      const int64_t oi = (int64_t)s * shard_len + e0;
+      if (vec_ok && cnt == E) {
+        store_words<E / 2>(out + oi, h);
+      } else {
+#pragma unroll
+        for (int i = 0; i < E; ++i)
+          if (i < cnt) store_scalar<O>(out + oi, i, h[i / 2] >> (16 * (i & 1)));
+      }
+      if (sec_out != nullptr && oi + cnt > sec_lo && oi < sec_lo + sec_len) {
+        const int64_t k0 = oi - sec_lo;
+#pragma unroll
+        for (int i = 0; i < E; ++i)
+          if (i < cnt && k0 + i >= 0 && k0 + i < sec_len) store_scalar<O>(sec_out + k0, i, h[i / 2] >> (16 * (i & 1)));
+      }
+    }
+    __syncthreads();  // every thread is done with this slot before it is refilled
+  }
   if (bad) raise_flag(flag, FLAG_BADCODE);
 }
 
