@@ -85,12 +85,15 @@ int zpp_dequantize(const void* codes, const void* absmax, int absmax_dtype, int6
 /* K4  gather-dequantize: the receive side of all_gather_qwz
  * (zs/collectives.py:264).  codes[s]/absmax[s] (host arrays of n_src device
  * pointers, local or NVLink peer) are decoded into out[s*shard_len ...].
- * rot staggers which source each warp starts with.  Optional hpZ
+ * rot staggers which source each warp starts with.  out_stride = elements
+ * between consecutive sources' segments in out (0 = shard_len; larger strides
+ * let a chunked caller gather piece k of every shard in place).  Optional hpZ
  * write-through: out elements [sec_lo, sec_lo+sec_len) are also written to
  * sec_out (NULL to skip). */
 int zpp_gather_dequantize(const void* const* codes, const void* const* absmax, int absmax_dtype, int n_src,
                           int rot, int64_t shard_len, int bits, int64_t block, void* out, int out_dtype,
-                          void* sec_out, int64_t sec_lo, int64_t sec_len, void* errflag, void* stream);
+                          int64_t out_stride, void* sec_out, int64_t sec_lo, int64_t sec_len, void* errflag,
+                          void* stream);
 
 /* K3  BlockCodec.reduce_final                      zs/collectives.py:71-75
  * out[i] = post_scale * fold_{s ascending}(+0.0, code_s[i]*scale_s) in f64. */
@@ -135,11 +138,11 @@ int zpp_comm_destroy(zpp_comm_t comm);
 /* qwZ all-gather, fused over NVLink (zs/collectives.py:244-282):
  * quantize this rank's shard into the symmetric buffer, world barrier, then
  * every rank decodes all W shards by peer loads straight into out
- * (W*shard_len elements).  Optional hpZ write-through of
- * out[sec_lo, sec_lo+sec_len) into sec_out. */
+ * (W*shard_len elements; out_stride as in zpp_gather_dequantize).  Optional
+ * hpZ write-through of out[sec_lo, sec_lo+sec_len) into sec_out. */
 int zpp_qwz_allgather(zpp_comm_t comm, size_t sym_offset, const void* shard, int dtype, int64_t shard_len, int bits,
-                      int64_t block, void* out, int out_dtype, void* sec_out, int64_t sec_lo, int64_t sec_len,
-                      void* errflag, void* stream);
+                      int64_t block, void* out, int out_dtype, int64_t out_stride, void* sec_out, int64_t sec_lo,
+                      int64_t sec_len, void* errflag, void* stream);
 
 /* hpZ secondary-partition all-gather inside the group over NVLink
  * (zs/collectives.py:202-241 with groups = PartitionSpec.groups()):

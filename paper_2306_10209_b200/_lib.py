@@ -36,7 +36,7 @@ SIGNATURES = {
     "zpp_swizzle_quantize": (c_int, [P, c_int, c_int64, c_int, c_int, c_int, c_int, c_int, c_int, c_int64,
                                      P, P, P, P]),
     "zpp_dequantize": (c_int, [P, P, c_int, c_int64, c_int, c_int64, P, c_int, P, P]),
-    "zpp_gather_dequantize": (c_int, [PP, PP, c_int, c_int, c_int, c_int64, c_int, c_int64, P, c_int,
+    "zpp_gather_dequantize": (c_int, [PP, PP, c_int, c_int, c_int, c_int64, c_int, c_int64, P, c_int, c_int64,
                                       P, c_int64, c_int64, P, P]),
     "zpp_dequant_reduce": (c_int, [PP, PP, c_int, c_int, c_int64, c_int, c_int64, P, c_int, c_double, P, P]),
     "zpp_dequant_reduce_quant": (c_int, [PP, PP, c_int, c_int, c_int64, c_int, c_int64, c_int, c_int64,
@@ -50,8 +50,8 @@ SIGNATURES = {
     "zpp_comm_sym_bytes": (c_size_t, [P]),
     "zpp_comm_barrier": (c_int, [P, c_int, c_int, P, P]),
     "zpp_comm_destroy": (c_int, [P]),
-    "zpp_qwz_allgather": (c_int, [P, c_size_t, P, c_int, c_int64, c_int, c_int64, P, c_int, P, c_int64, c_int64,
-                                  P, P]),
+    "zpp_qwz_allgather": (c_int, [P, c_size_t, P, c_int, c_int64, c_int, c_int64, P, c_int, c_int64, P, c_int64,
+                                  c_int64, P, P]),
     "zpp_hpz_allgather": (c_int, [P, c_size_t, c_int64, c_int, P, P, P]),
     "zpp_qgz_reduce_scatter": (c_int, [P, c_size_t, P, c_int, c_int64, c_int, c_int, c_int, c_int64, c_int,
                                        c_int64, P, c_int, P, P]),

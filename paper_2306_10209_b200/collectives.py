@@ -309,8 +309,8 @@ def _gather_decode(qs: list[QuantizedTensor], out_dtype: torch.dtype) -> torch.T
     cp, _k1 = _lib.ptr_array([q.codes.data_ptr() for q in qs])
     ap, _k2 = _lib.ptr_array([q.absmax.data_ptr() for q in qs])
     _lib.check(_lib.load().zpp_gather_dequantize(cp, ap, q0.absmax_code, len(qs), 0, n, q0.config.bit_width,
-                                                 q0.config.block_size, out.data_ptr(), dtype_code(out_dtype), None,
-                                                 0, 0, f.data_ptr(), stream_ptr()), "all_gather_qwz")
+                                                 q0.config.block_size, out.data_ptr(), dtype_code(out_dtype), n,
+                                                 None, 0, 0, f.data_ptr(), stream_ptr()), "all_gather_qwz")
     check_flag(f, "all_gather_qwz")
     return out
 

@@ -146,8 +146,9 @@ int launch_quantize(const void* x, int dtype, const AddrSpec& a, int64_t n_out, 
 
 template <int BITS, typename A, typename O>
 static int run_gather(const SrcTable& t, int n_src, int rot, int64_t shard_len, int64_t block, void* out,
-                      void* sec_out, int64_t sec_lo, int64_t sec_len, uint32_t* flag, cudaStream_t st) {
-  const int vec_ok = aligned16(out) && (shard_len % 8 == 0) &&
+                      void* sec_out, int64_t sec_lo, int64_t sec_len, uint32_t* flag, cudaStream_t st,
+                      int64_t out_stride) {
+  const int vec_ok = aligned16(out) && (shard_len % 8 == 0) && (out_stride % 8 == 0) &&
                      (sec_out == nullptr || (aligned16(sec_out) && sec_lo % 8 == 0));
   constexpr bool k16 = sizeof(O) == 2 && std::is_same<A, float>::value;
   if constexpr (k16) {
@@ -166,7 +167,7 @@ static int run_gather(const SrcTable& t, int n_src, int rot, int64_t shard_len, 
     auto k = dequant16_pipe_kernel<BITS, O, P>;                                                        \
     const int grid = grid_for(k, 256, tiles);                                                          \
     k<<<grid, 256, 0, st>>>(t, n_src, rot, shard_len, block, reinterpret_cast<O*>(out),                \
-                            reinterpret_cast<O*>(sec_out), sec_lo, sec_len, vec_ok, flag);            \
+                            reinterpret_cast<O*>(sec_out), sec_lo, sec_len, vec_ok, flag, out_stride);            \
     return check_cuda(cudaGetLastError(), "dequant16_pipe_kernel launch");                             \
   }
       // default: TMA bulk pipeline (ZPP_GATHER_MODE=pipe selects the per-thread cp.async ring)
@@ -188,7 +189,7 @@ static int run_gather(const SrcTable& t, int n_src, int rot, int64_t shard_len, 
     const int grid = (int)std::min<int64_t>((int64_t)sm_count() * std::max(occ, 1),                  \
                                             ceil_div(units, TU) * n_src);                              \
     k<<<grid, 256, smem, st>>>(t, n_src, rot, shard_len, block, reinterpret_cast<O*>(out),             \
-                            reinterpret_cast<O*>(sec_out), sec_lo, sec_len, vec_ok, flag);            \
+                            reinterpret_cast<O*>(sec_out), sec_lo, sec_len, vec_ok, flag, out_stride);            \
     return check_cuda(cudaGetLastError(), "dequant16_tma_kernel launch");                              \
   }
         if (tma_cfg == 1) ZPP_TMA(8, 512)
@@ -208,7 +209,7 @@ static int run_gather(const SrcTable& t, int n_src, int rot, int64_t shard_len, 
       const int64_t tiles = ceil_div(ceil_div(shard_len, 128 / BITS), 32 * (BITS == 8 ? 2 : 1)) * n_src;
       const int grid = grid_for(k, 256, ceil_div(tiles, 8));
       k<<<grid, 256, 0, st>>>(t, n_src, rot, shard_len, block, reinterpret_cast<O*>(out),
-                              reinterpret_cast<O*>(sec_out), sec_lo, sec_len, vec_ok, flag);
+                              reinterpret_cast<O*>(sec_out), sec_lo, sec_len, vec_ok, flag, out_stride);
       return check_cuda(cudaGetLastError(), "dequant16_kernel launch");
     }
   }
@@ -216,19 +217,22 @@ static int run_gather(const SrcTable& t, int n_src, int rot, int64_t shard_len, 
   const int64_t tiles = ceil_div(ceil_div(shard_len, 8), 32 * 4) * n_src;
   const int grid = grid_for(k, 256, ceil_div(tiles, 8));
   k<<<grid, 256, 0, st>>>(t, n_src, rot, shard_len, block, reinterpret_cast<O*>(out), reinterpret_cast<O*>(sec_out),
-                          sec_lo, sec_len, vec_ok, flag);
+                          sec_lo, sec_len, vec_ok, flag, out_stride);
   return check_cuda(cudaGetLastError(), "dequant_gather_kernel launch");
 }
 
 int launch_gather_dequant(const void* const* codes, const void* const* absmax, int absmax_dtype, int n_src, int rot,
                           int64_t shard_len, int bits, int64_t block, void* out, int out_dtype, void* sec_out,
-                          int64_t sec_lo, int64_t sec_len, uint32_t* flag, cudaStream_t st) {
+                          int64_t sec_lo, int64_t sec_len, uint32_t* flag, cudaStream_t st, int64_t out_stride) {
   if (shard_len == 0) return ZPP_OK;
+  if (out_stride == 0) out_stride = shard_len;
+  if (out_stride < shard_len) return fail(ZPP_ERR_VALIDATION, "out_stride smaller than shard_len");
   SrcTable t;
   int rc = fill_table(t, codes, absmax, n_src);
   if (rc) return rc;
   rot = ((rot % n_src) + n_src) % n_src;
-  ZPP_DISPATCH_BA_O(run_gather, t, n_src, rot, shard_len, block, out, sec_out, sec_lo, sec_len, flag, st);
+  ZPP_DISPATCH_BA_O(run_gather, t, n_src, rot, shard_len, block, out, sec_out, sec_lo, sec_len, flag, st,
+                    out_stride);
 }
 
 }  // namespace zpp
@@ -302,19 +306,19 @@ int zpp_dequantize(const void* codes, const void* absmax, int absmax_dtype, int6
   const void* c[1] = {codes};
   const void* a[1] = {absmax};
   return launch_gather_dequant(c, a, absmax_dtype, 1, 0, n, bits, block, out, out_dtype, nullptr, 0, 0,
-                               reinterpret_cast<uint32_t*>(errflag), reinterpret_cast<cudaStream_t>(stream));
+                               reinterpret_cast<uint32_t*>(errflag), reinterpret_cast<cudaStream_t>(stream), n);
 }
 
 int zpp_gather_dequantize(const void* const* codes, const void* const* absmax, int absmax_dtype, int n_src, int rot,
-                          int64_t shard_len, int bits, int64_t block, void* out, int out_dtype, void* sec_out,
-                          int64_t sec_lo, int64_t sec_len, void* errflag, void* stream) {
+                          int64_t shard_len, int bits, int64_t block, void* out, int out_dtype, int64_t out_stride,
+                          void* sec_out, int64_t sec_lo, int64_t sec_len, void* errflag, void* stream) {
   int rc = check_cfg(bits, block);
   if (rc || (rc = check_dtype(out_dtype))) return rc;
   if (shard_len < 0 || !codes || !absmax) return fail(ZPP_ERR_VALIDATION, "bad arguments");
   if (shard_len > 0 && !out) return fail(ZPP_ERR_VALIDATION, "null pointer");
   return launch_gather_dequant(codes, absmax, absmax_dtype, n_src, rot, shard_len, bits, block, out, out_dtype,
                                sec_out, sec_lo, sec_len, reinterpret_cast<uint32_t*>(errflag),
-                               reinterpret_cast<cudaStream_t>(stream));
+                               reinterpret_cast<cudaStream_t>(stream), out_stride);
 }
 
 int zpp_dequant_reduce(const void* const* codes, const void* const* absmax, int absmax_dtype, int n_src, int64_t n,

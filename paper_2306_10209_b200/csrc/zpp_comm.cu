@@ -241,8 +241,8 @@ size_t zpp_qwz_sym_bytes(int64_t shard_len, int bits, int64_t block, int world) 
 }
 
 int zpp_qwz_allgather(zpp_comm_t c, size_t sym_offset, const void* shard, int dtype, int64_t shard_len, int bits,
-                      int64_t block, void* out, int out_dtype, void* sec_out, int64_t sec_lo, int64_t sec_len,
-                      void* errflag, void* stream) {
+                      int64_t block, void* out, int out_dtype, int64_t out_stride, void* sec_out, int64_t sec_lo,
+                      int64_t sec_len, void* errflag, void* stream) {
   int rc = comm_ok(c);
   if (rc) return rc;
   if ((bits != 4 && bits != 8) || block < 8 || block % 8) return fail(ZPP_ERR_CONFIG, "bad quant config");
@@ -270,7 +270,7 @@ int zpp_qwz_allgather(zpp_comm_t c, size_t sym_offset, const void* shard, int dt
     absmax[r] = c->peers[r] + base + abs_off;
   }
   return launch_gather_dequant(codes, absmax, dtype == ZPP_F64 ? ZPP_F64 : ZPP_F32, c->world, c->rank, shard_len,
-                               bits, block, out, out_dtype, sec_out, sec_lo, sec_len, flag, st);
+                               bits, block, out, out_dtype, sec_out, sec_lo, sec_len, flag, st, out_stride);
 }
 
 // ---------------------------------------------------------------------------

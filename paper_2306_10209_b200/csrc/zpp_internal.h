@@ -28,7 +28,8 @@ int launch_quantize(const void* x, int dtype, const AddrSpec& a, int64_t n_out, 
                     uint8_t* codes, void* absmax, uint32_t* flag, cudaStream_t st);
 int launch_gather_dequant(const void* const* codes, const void* const* absmax, int absmax_dtype, int n_src,
                           int rot, int64_t shard_len, int bits, int64_t block, void* out, int out_dtype,
-                          void* sec_out, int64_t sec_lo, int64_t sec_len, uint32_t* flag, cudaStream_t st);
+                          void* sec_out, int64_t sec_lo, int64_t sec_len, uint32_t* flag, cudaStream_t st,
+                          int64_t out_stride = 0);
 int launch_dequant_reduce(const void* const* codes, const void* const* absmax, int absmax_dtype, int n_src,
                           int64_t n, int bits, int64_t block, void* out, int out_dtype, double post_scale,
                           uint32_t* flag, cudaStream_t st, bool validate = true);

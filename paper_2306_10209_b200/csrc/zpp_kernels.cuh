@@ -581,7 +581,8 @@ __device__ __forceinline__ void store_words(void* dst, const uint32_t (&h)[N]) {
 template <int BITS, typename O>
 __global__ void __launch_bounds__(256, 4)
 dequant16_kernel(SrcTable src, int n_src, int rot, int64_t shard_len, int64_t B, O* __restrict__ out,
-                 O* __restrict__ sec_out, int64_t sec_lo, int64_t sec_len, int vec_ok, uint32_t* __restrict__ flag) {
+                 O* __restrict__ sec_out, int64_t sec_lo, int64_t sec_len, int vec_ok, uint32_t* __restrict__ flag,
+                 int64_t out_stride) {
   constexpr int E = Unit16B<BITS>::E;
   constexpr int U = BITS == 8 ? 2 : 1;  // 16-byte code loads per lane per tile
   constexpr int TU = 32 * U;            // units per warp tile
@@ -602,7 +603,7 @@ dequant16_kernel(SrcTable src, int n_src, int rot, int64_t shard_len, int64_t B,
     const int t0 = t * TU;
     const uint4* cs = reinterpret_cast<const uint4*>(src.codes[s]);
     const float* am = reinterpret_cast<const float*>(src.absmax[s]);
-    const int64_t obase = (int64_t)s * shard_len;
+    const int64_t obase = (int64_t)s * out_stride;
     // tile fully inside the shard, vector-aligned and not touching the hpZ
     // secondary range: branch-free fast path
     const int64_t te0 = obase + (int64_t)t0 * E, te1 = te0 + (int64_t)TU * E;
@@ -670,7 +671,7 @@ template <int BITS, typename O, int PIPE>
 __global__ void __launch_bounds__(256, 4)
 dequant16_pipe_kernel(SrcTable src, int n_src, int rot, int64_t shard_len, int64_t B, O* __restrict__ out,
                       O* __restrict__ sec_out, int64_t sec_lo, int64_t sec_len, int vec_ok,
-                      uint32_t* __restrict__ flag) {
+                      uint32_t* __restrict__ flag, int64_t out_stride) {
   constexpr int E = Unit16B<BITS>::E;
   __shared__ uint4 ring[PIPE][256];
   const int tid = threadIdx.x;
@@ -716,7 +717,7 @@ dequant16_pipe_kernel(SrcTable src, int n_src, int rot, int64_t shard_len, int64
     uint32_t h[E / 2];
     decode16_any<BITS, O>(w, m, h);
     const int cnt = (int)min((int64_t)E, shard_len - e0);
-    const int64_t oi = (int64_t)s * shard_len + e0;
+    const int64_t oi = (int64_t)s * out_stride + e0;
     if (vec_ok && cnt == E) {
       store_words<E / 2>(out + oi, h);
     } else {
@@ -777,7 +778,7 @@ template <int BITS, typename O, int STAGES, int TILE_U>
 __global__ void __launch_bounds__(256)
 dequant16_tma_kernel(SrcTable src, int n_src, int rot, int64_t shard_len, int64_t B, O* __restrict__ out,
                      O* __restrict__ sec_out, int64_t sec_lo, int64_t sec_len, int vec_ok,
-                     uint32_t* __restrict__ flag) {
+                     uint32_t* __restrict__ flag, int64_t out_stride) {
   constexpr int E = Unit16B<BITS>::E;
   constexpr int UPT = TILE_U / 256;  // units per thread per tile
   extern __shared__ __align__(128) uint8_t dsm[];  // [STAGES][TILE_U] uint4 ring, then STAGES mbarriers
@@ -836,7 +837,7 @@ dequant16_tma_kernel(SrcTable src, int n_src, int rot, int64_t shard_len, int64_
       uint32_t h[E / 2];
       decode16_any<BITS, O>(w, m, h);
       const int cnt = (int)min((int64_t)E, shard_len - e0);
-      const int64_t oi = (int64_t)s * shard_len + e0;
+      const int64_t oi = (int64_t)s * out_stride + e0;
       if (vec_ok && cnt == E) {
         store_words<E / 2>(out + oi, h);
       } else {
@@ -922,7 +923,7 @@ template <int BITS, typename A, typename O>
 __global__ void __launch_bounds__(256)
 dequant_gather_kernel(SrcTable src, int n_src, int rot, int64_t shard_len, int64_t B, O* __restrict__ out,
                       O* __restrict__ sec_out, int64_t sec_lo, int64_t sec_len, int vec_ok,
-                      uint32_t* __restrict__ flag) {
+                      uint32_t* __restrict__ flag, int64_t out_stride) {
   constexpr int U = 4;
   using CW = typename std::conditional<BITS == 8, uint2, uint32_t>::type;
   const int lane = threadIdx.x & 31;
@@ -953,7 +954,7 @@ dequant_gather_kernel(SrcTable src, int n_src, int rot, int64_t shard_len, int64
       double v[8];
       decode8<BITS>(reinterpret_cast<const uint8_t*>(&w[u]), sc, v, bad);
       const int cnt = (int)min((int64_t)8, shard_len - e);
-      const int64_t oi = (int64_t)s * shard_len + e;
+      const int64_t oi = (int64_t)s * out_stride + e;
       store8<O>(out + oi, v, cnt, vec_ok);
       if (sec_out != nullptr && oi + cnt > sec_lo && oi < sec_lo + sec_len) {
 #pragma unroll

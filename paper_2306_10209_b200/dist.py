@@ -142,20 +142,25 @@ class Communicator:
     # -- collectives ---------------------------------------------------------
 
     def qwz_allgather(self, shard: torch.Tensor, out: torch.Tensor | None = None,
-                      out_dtype: torch.dtype = torch.float16, write_secondary: bool = False) -> torch.Tensor:
+                      out_dtype: torch.dtype = torch.float16, write_secondary: bool = False,
+                      out_stride: int = 0) -> torch.Tensor:
         """qwZ: every rank ends with the concatenation (rank order) of every
-        rank's dequantize(quantize(shard)) -- zs/collectives.py:244-282."""
+        rank's dequantize(quantize(shard)) -- zs/collectives.py:244-282.
+
+        ``out_stride`` (elements between consecutive ranks' segments, default
+        the shard length) lets a caller gather piece k of every shard in place."""
         n = int(shard.numel())
-        if n != self.qwz_shard:
+        if n > self.qwz_shard:
             raise ValidationError(f"shard has {n} elements, communicator was sized for {self.qwz_shard}")
+        stride = out_stride or n
         if out is None:
-            out = torch.empty(n * self.world, dtype=out_dtype, device=shard.device)
+            out = torch.empty(stride * (self.world - 1) + n, dtype=out_dtype, device=shard.device)
         sec_ptr, sec_lo, sec_len = None, 0, 0
         if write_secondary:
             if self._secondary is None:
                 raise ValidationError("communicator has no hpZ secondary region")
-            if out.dtype != self.hpz_dtype:
-                raise ValidationError("secondary partition dtype must match the gather output dtype")
+            if out.dtype != self.hpz_dtype or stride != n:
+                raise ValidationError("secondary write-through needs an unstrided gather of the hpZ dtype")
             spec = PartitionSpec(total_elems=n * self.world, world=self.world, group_size=self.group_size)
             sec_lo, sec_hi = spec.secondary_range(self.rank)
             if sec_hi - sec_lo != self.hpz_sec:
@@ -164,9 +169,47 @@ class Communicator:
             sec_ptr = self._secondary.data_ptr()
         _lib.check(self.lib.zpp_qwz_allgather(self.handle, self.layout.qwz, shard.data_ptr(), dtype_code(shard.dtype),
                                               n, self.qwz_cfg.bit_width, self.qwz_cfg.block_size, out.data_ptr(),
-                                              dtype_code(out.dtype), sec_ptr, sec_lo, sec_len, self.flag.data_ptr(),
-                                              stream_ptr()), "qwz_allgather")
+                                              dtype_code(out.dtype), stride, sec_ptr, sec_lo, sec_len,
+                                              self.flag.data_ptr(), stream_ptr()), "qwz_allgather")
         return out
+
+    def qwz_allgather_host(self, h_shard: torch.Tensor, h_out: torch.Tensor, chunks: int = 8,
+                           d_shard: torch.Tensor | None = None, d_out: torch.Tensor | None = None):
+        """qwZ between HOST buffers with transfer/compute overlap.
+
+        The shard is split into ``chunks`` block-aligned pieces; piece k is one
+        fused sub-collective (quantize piece k of every rank's shard, gather it
+        in place), so H2D of piece k+1, the collective on piece k and D2H of
+        piece k-1 run concurrently on three streams.  h_shard / h_out should be
+        pinned.  Same values as ``qwz_allgather`` (blocks never straddle pieces)."""
+        n = int(h_shard.numel())
+        blk = self.qwz_cfg.block_size
+        per = -(-(-(-n // chunks)) // blk) * blk
+        if d_shard is None:
+            d_shard = torch.empty(n, dtype=h_shard.dtype, device=device())
+        if d_out is None:
+            d_out = torch.empty(n * self.world, dtype=h_out.dtype, device=device())
+        if not hasattr(self, "_h2d"):
+            self._h2d, self._d2h = torch.cuda.Stream(), torch.cuda.Stream()
+        main = torch.cuda.current_stream()
+        self._h2d.wait_stream(main)
+        self._d2h.wait_stream(main)
+        pieces = [(k, min(per, n - k)) for k in range(0, n, per)]
+        for k, cl in pieces:
+            with torch.cuda.stream(self._h2d):
+                d_shard[k:k + cl].copy_(h_shard[k:k + cl], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record()
+            main.wait_event(ev)
+            self.qwz_allgather(d_shard[k:k + cl], out=d_out[k:], out_stride=n)
+            done = torch.cuda.Event()
+            done.record(main)
+            with torch.cuda.stream(self._d2h):
+                self._d2h.wait_event(done)
+                for r in range(self.world):
+                    h_out[r * n + k:r * n + k + cl].copy_(d_out[r * n + k:r * n + k + cl], non_blocking=True)
+        main.wait_stream(self._d2h)
+        return h_out
 
     @property
     def secondary(self) -> torch.Tensor:

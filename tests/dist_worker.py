@@ -62,6 +62,13 @@ def main():
         g = comm.hpz_allgather()
         comm.check()
         check(f"hpz gather it{it}", np.array_equal(g.cpu().numpy(), want16))
+    # host-buffer API with transfer/compute overlap (chunked sub-collectives)
+    h_in = torch.from_numpy(shards[rank]).pin_memory()
+    h_out = torch.empty(total, dtype=torch.float16).pin_memory()
+    comm.qwz_allgather_host(h_in, h_out, chunks=3)
+    torch.cuda.synchronize()
+    comm.check()
+    check("qwz host chunked", np.array_equal(h_out.numpy(), want16))
     # f32 output of the same gather
     out32 = comm.qwz_allgather(mine, out_dtype=torch.float32)
     comm.check()

@@ -28,6 +28,10 @@ def test_world1_collectives():
         assert np.array_equal(out.cpu().numpy(), want.astype(np.float16))
         assert np.array_equal(comm.secondary.cpu().numpy(), want.astype(np.float16))
         assert np.array_equal(comm.hpz_allgather().cpu().numpy(), want.astype(np.float16))
+    h_out = torch.empty(n, dtype=torch.float16).pin_memory()
+    comm.qwz_allgather_host(torch.from_numpy(x).pin_memory(), h_out, chunks=4)
+    torch.cuda.synchronize()
+    assert np.array_equal(h_out.numpy(), want.astype(np.float16))
     g = (np.random.default_rng(1).normal(size=4096) * 1e-3).astype(np.float32)
     ref = O.qgz_2hop([g.astype(np.float64)], 1, 1, 2, 4, 512)[0]
     for _ in range(3):
@@ -40,5 +44,5 @@ def test_world1_collectives():
     with pytest.raises(zpp.ValidationError):
         comm.check()
     with pytest.raises(zpp.ValidationError):
-        comm.qwz_allgather(torch.zeros(10, device="cuda", dtype=torch.float16))
+        comm.qwz_allgather(torch.zeros(n + 8, device="cuda", dtype=torch.float16))
     comm.close()
