@@ -50,10 +50,13 @@ from .collectives import (
     all_gather_baseline,
     all_gather_qwz,
     as_codec,
+    qgz_1hop,
     qgz_2hop,
     reduce_scatter_ring,
+    reduce_scatter_ring_naive_quant,
     reorder_mapping,
 )
+from .accounting import BWD_GATHER, FWD_GATHER, GRAD_REDUCE, StepConfig, step_volumes
 
 __version__ = "0.1.0"
 
@@ -66,6 +69,7 @@ __all__ = [
     "PartitionSpec", "build_partitions",
     "BlockCodec", "PassthroughCodec", "WirePayload", "as_codec", "GatherResult", "ReduceResult",
     "ReorderPermutation", "all_gather_baseline", "all_gather_qwz", "reduce_scatter_ring", "reorder_mapping",
-    "qgz_2hop",
+    "qgz_2hop", "qgz_1hop", "reduce_scatter_ring_naive_quant",
+    "StepConfig", "step_volumes", "FWD_GATHER", "BWD_GATHER", "GRAD_REDUCE",
     "__version__",
 ]

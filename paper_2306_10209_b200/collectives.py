@@ -48,7 +48,17 @@ from .quantizer import (
     quantize,
     stream_ptr,
 )
-from .topology import INTER, INTRA, ClusterTopology, CollectiveTrace, TrafficLedger, account_phase, span_class
+from .accounting import (
+    account_allgather,
+    account_qgz,
+    account_qgz_1hop,
+    account_qwz,
+    account_ring,
+    account_ring_naive_quant,
+)
+from .accounting import encode_sizes as _encode_sizes  # noqa: F401  (re-exported for callers/tests)
+from .accounting import volume_valid_adjust as _volume_valid_adjust  # noqa: F401
+from .topology import ClusterTopology, CollectiveTrace, TrafficLedger
 
 FP16_BYTES = 2
 
@@ -193,23 +203,6 @@ def _check_equal_inputs(tensors, world):
     return n
 
 
-def _volume_valid_adjust(ledger, label, cls, payload, metadata, padding, payload_valid):
-    """zs/collectives.py:180-183."""
-    extra = payload - min(payload, payload_valid)
-    ledger.record_volume(label, cls, payload=payload - extra, metadata=metadata, padding=padding + extra)
-
-
-def _encode_sizes(codec, k: int):
-    """zs/collectives.py:186-195."""
-    if codec.is_passthrough:
-        return k * FP16_BYTES, 0, 0
-    cfg = codec.cfg
-    eff = effective_block(cfg, k)
-    blocks = math.ceil(k / eff)
-    payload = math.ceil(k * cfg.bit_width / 8)
-    return payload, blocks * 2, blocks * eff * cfg.bit_width // 8 - payload
-
-
 def _check_scheduler(scheduler):
     if scheduler not in ("serial", "threads"):
         raise ValidationError(f"unknown scheduler {scheduler!r}")
@@ -249,18 +242,12 @@ def all_gather_baseline(shards, topo: ClusterTopology, ledger: TrafficLedger, *,
     if any(len(s) != shard_len for s in shards):
         raise ValidationError("shards must have equal length")
     web = shards[0].wire_element_bytes
-    trace = CollectiveTrace(label=label)
-    account_phase(ledger, trace, topo, label, "allgather",
-                  ((r, m, shard_len * web, 0, 0) for r in range(world) for m in groups[group_of[r]]))
+    trace = account_allgather(ledger, topo, label, shard_len, web, groups=groups, valid_elems=valid_elems)
     outs = []
     for members in groups:
         cat = torch.cat([shards[m].cuda_values() for m in members]) if members else None
         outs.append(_wrap(cat, web))
     gathered = [outs[group_of[r]] for r in range(world)]
-    cls = INTER if any(span_class(m, topo) == INTER for m in groups) else INTRA
-    gathered_elems = shard_len * len(groups[0])
-    valid = gathered_elems if valid_elems is None else valid_elems
-    _volume_valid_adjust(ledger, label, cls, gathered_elems * web, 0, 0, valid * web)
     return GatherResult(gathered=gathered, trace=trace)
 
 
@@ -276,20 +263,11 @@ def all_gather_qwz(shards, codec, topo: ClusterTopology, ledger: TrafficLedger, 
     shards = [as_flat(s) for s in shards]
     shard_len = _check_equal_inputs(shards, world)
     encoded = [codec.encode(s) for s in shards]
-    trace = CollectiveTrace(label=label)
-    acct = [codec.accounting(wp) for wp in encoded]
-    account_phase(ledger, trace, topo, label, "allgather",
-                  ((r, d, *acct[r]) for r in range(world) for d in range(world)))
+    trace = account_qwz(ledger, topo, label, codec, shard_len, valid_elems=valid_elems)
     if codec.is_passthrough:
         out = torch.cat([codec.decode(wp) for wp in encoded])
     else:
         out = _gather_decode([wp.data for wp in encoded], codec.out_dtype)
-    payload = sum(a[0] for a in acct)
-    metadata = sum(a[1] for a in acct)
-    padding = sum(a[2] for a in acct)
-    valid = shard_len * world if valid_elems is None else valid_elems
-    _volume_valid_adjust(ledger, label, span_class(range(world), topo), payload, metadata, padding,
-                         codec.payload_bytes_for(valid))
     g = _wrap(out)
     return GatherResult(gathered=[g] * world, trace=trace, codec_depth=max(wp.depth for wp in encoded),
                         quantized=None if codec.is_passthrough else [wp.data for wp in encoded])
@@ -332,10 +310,7 @@ def reduce_scatter_ring(inputs, topo: ClusterTopology, ledger: TrafficLedger, *,
         raise ValidationError(f"input length {n} not divisible by world {world}")
     chunk = n // world
     web = inputs[0].wire_element_bytes
-    trace = CollectiveTrace(label=label)
-    for step in range(world - 1):
-        account_phase(ledger, trace, topo, label, f"ring{step}",
-                      ((r, (r + 1) % world, chunk * web, 0, 0) for r in range(world)))
+    trace = account_ring(ledger, topo, label, n, web, valid_elems=valid_elems)
     vals = [t.cuda_values().to(torch.float64) for t in inputs]
     shards = []
     for r in range(world):
@@ -346,8 +321,6 @@ def reduce_scatter_ring(inputs, topo: ClusterTopology, ledger: TrafficLedger, *,
             for v in vals:
                 total += v[r * chunk:(r + 1) * chunk]
         shards.append(_wrap(total, web))
-    valid = n if valid_elems is None else valid_elems
-    _volume_valid_adjust(ledger, label, span_class(range(world), topo), n * web, 0, 0, valid * web)
     return ReduceResult(shards=shards, trace=trace)
 
 
@@ -410,25 +383,17 @@ def qgz_2hop(inputs, codec, topo: ClusterTopology, ledger: TrafficLedger, *, sta
     codec.check_slice_len(L)
     if not codec.is_passthrough and (codec.cfg.mode != "blocked" or intra.cfg.mode != "blocked"):
         raise ValidationError("slice_blocks requires block-aligned bounds")  # what the reference hits
-    trace = CollectiveTrace(label=label)
+    trace = account_qgz(ledger, topo, label, codec, intra, n, s, valid_elems=valid_elems)
     if codec.is_passthrough:
-        shards = _qgz_protocol(inputs, codec, intra, topo, ledger, trace, label, s, L, reorder)
+        shards = _qgz_protocol(inputs, codec, intra, topo, s, L, reorder)
         depth, bounds = 0, None
     else:
-        shards, bounds = _qgz_kernels(inputs, codec, intra, topo, ledger, trace, label, s, L, reorder,
-                                      collect_bounds)
+        shards, bounds = _qgz_kernels(inputs, codec, intra, topo, s, L, reorder, collect_bounds)
         depth = 2
-    valid = n if valid_elems is None else valid_elems
-    pb1, mb1, padb1 = _encode_sizes(intra, y * L)
-    _volume_valid_adjust(ledger, label + "/intra", INTRA, x * x * s * pb1, x * x * s * mb1, x * x * s * padb1,
-                         x * intra.payload_bytes_for(valid))
-    pb2, mb2, padb2 = _encode_sizes(codec, L)
-    _volume_valid_adjust(ledger, label, INTER if y > 1 else INTRA, x * y * s * pb2, x * y * s * mb2,
-                         x * y * s * padb2, codec.payload_bytes_for(valid))
     return ReduceResult(shards=shards, trace=trace, codec_depth=depth, error_bounds=bounds)
 
 
-def _qgz_kernels(inputs, codec, intra, topo, ledger, trace, label, s, L, reorder, collect_bounds):
+def _qgz_kernels(inputs, codec, intra, topo, s, L, reorder, collect_bounds):
     x, y = topo.gpus_per_node, topo.nodes
     world = x * y
     lib = _lib.load()
@@ -449,20 +414,12 @@ def _qgz_kernels(inputs, codec, intra, topo, ledger, trace, label, s, L, reorder
                                                 icfg.bit_width, icfg.block_size, q.codes.data_ptr(),
                                                 q.absmax.data_ptr(), f.data_ptr(), stream_ptr()), "qgz_2hop")
             sends.append([q.slice_blocks(j * msg, msg) for j in range(x)])
-        one_intra = sends[0][0]
-        account_phase(ledger, trace, topo, label, f"s{st}.intra",
-                      ((r, (r // x) * x + j, one_intra.payload_bytes, one_intra.metadata_bytes,
-                        one_intra.padding_bytes) for r in range(world) for j in range(x)))
         # K2 at every receiver: messages in ascending local source order
         fused = []
         for r in range(world):
             node, loc = divmod(r, x)
             hop1 = [sends[node * x + j][loc] for j in range(x)]
             fused.append(fused_dequant_reduce_quant(hop1, ocfg, flag=f))
-        seg0 = fused[0].slice_blocks(0, L)
-        account_phase(ledger, trace, topo, label, f"s{st}.inter",
-                      ((r, c * x + (r % x), seg0.payload_bytes, seg0.metadata_bytes, seg0.padding_bytes)
-                       for r in range(world) for c in range(y)))
         # K3 at every receiver: segments in ascending node order
         for r in range(world):
             node, loc = divmod(r, x)
@@ -482,7 +439,7 @@ def _qgz_kernels(inputs, codec, intra, topo, ledger, trace, label, s, L, reorder
     return [_wrap(o) for o in outs], bounds
 
 
-def _qgz_protocol(inputs, codec, intra, topo, ledger, trace, label, s, L, reorder):
+def _qgz_protocol(inputs, codec, intra, topo, s, L, reorder):
     """Codec-protocol route (used with PassthroughCodec), zs/collectives.py:502-544."""
     x, y = topo.gpus_per_node, topo.nodes
     world = x * y
@@ -498,8 +455,6 @@ def _qgz_protocol(inputs, codec, intra, topo, ledger, trace, label, s, L, reorde
             for j in range(x):
                 parts = [vals[r][int(resid_at[j * y + c]) * part + st * L:][:L] for c in range(y)]
                 sent[(r, node * x + j)] = intra.encode(torch.cat(parts))
-        account_phase(ledger, trace, topo, label, f"s{st}.intra",
-                      ((src, dst, *intra.accounting(wp)) for (src, dst), wp in sent.items()))
         fused = {}
         for r in range(world):
             node = r // x
@@ -509,10 +464,68 @@ def _qgz_protocol(inputs, codec, intra, topo, ledger, trace, label, s, L, reorde
             loc = r % x
             for c in range(y):
                 segs[(r, c * x + loc)] = codec.slice(fused[r], c * L, L)
-        account_phase(ledger, trace, topo, label, f"s{st}.inter",
-                      ((src, dst, *codec.accounting(wp)) for (src, dst), wp in segs.items()))
         for r in range(world):
             loc = r % x
             received = [segs[(c * x + loc, r)] for c in range(y)]
             outs[r][st * L:(st + 1) * L] = codec.reduce_final(received)
     return [_wrap(o) for o in outs]
+
+
+# ---------------------------------------------------------------------------
+# comparators the paper argues against (zs/collectives.py:334-381, :420-461)
+
+
+def qgz_1hop(inputs, codec, topo: ClusterTopology, ledger: TrafficLedger, *, label="reduce_scatter",
+             valid_elems=None, scheduler="serial"):
+    """Single all-to-all quantized reduce-scatter (zs/collectives.py:420-461):
+    each rank encodes every destination chunk once, destinations fold in
+    ascending source order.  One codec pass, but X-fold cross-node volume."""
+    _check_scheduler(scheduler)
+    codec = as_codec(codec)
+    world = topo.world
+    inputs = [as_flat(t) for t in inputs]
+    n = _check_equal_inputs(inputs, world)
+    if n % world:
+        raise ValidationError(f"input length {n} not divisible by world {world}")
+    chunk = n // world
+    trace = account_qgz_1hop(ledger, topo, label, codec, n, valid_elems=valid_elems)
+    vals = [t.cuda_values() for t in inputs]
+    sent = [[codec.encode(vals[r][d * chunk:(d + 1) * chunk]) for d in range(world)] for r in range(world)]
+    shards = [_wrap(codec.reduce_final([sent[r][d] for r in range(world)])) for d in range(world)]
+    depth = max(wp.depth for row in sent for wp in row)
+    return ReduceResult(shards=shards, trace=trace, codec_depth=depth)
+
+
+def reduce_scatter_ring_naive_quant(inputs, codec, topo: ClusterTopology, ledger: TrafficLedger, *,
+                                    label="reduce_scatter", scheduler="serial"):
+    """Ring reduce-scatter that re-quantizes the running partial at every hop
+    (zs/collectives.py:334-381): codec depth world-1, the error the two-hop
+    scheme removes."""
+    _check_scheduler(scheduler)
+    codec = as_codec(codec)
+    world = topo.world
+    inputs = [as_flat(t) for t in inputs]
+    n = _check_equal_inputs(inputs, world)
+    if n % world:
+        raise ValidationError(f"input length {n} not divisible by world {world}")
+    chunk = n // world
+    trace = account_ring_naive_quant(ledger, topo, label, codec, n)
+    vals = [t.cuda_values().to(torch.float64) for t in inputs]
+    shards, depth = [], 0
+    for dst in range(world):
+        # the partial for chunk dst starts at rank dst+1 and travels the ring to dst
+        order = [(dst + 1 + k) % world for k in range(world)]
+        wp = None
+        for r in order[:-1]:
+            piece = vals[r][dst * chunk:(dst + 1) * chunk]
+            if wp is None:
+                wp = codec.encode(piece.clone())
+            else:
+                wp = codec.encode(codec.decode(wp).to(torch.float64) + piece, prior_depth=wp.depth)
+        own = vals[dst][dst * chunk:(dst + 1) * chunk]
+        if wp is None:
+            shards.append(_wrap(own.clone()))
+        else:
+            shards.append(_wrap(codec.decode(wp).to(torch.float64) + own))
+            depth = max(depth, wp.depth)
+    return ReduceResult(shards=shards, trace=trace, codec_depth=depth)

@@ -181,6 +181,21 @@ class QuantizedTensor:
         scales16 = self.scales.cpu().numpy().astype(np.float16).tobytes()
         return header + scales16 + self.codes.cpu().numpy().tobytes()
 
+    @classmethod
+    def from_bytes(cls, raw: bytes) -> "QuantizedTensor":
+        """Parse the canonical wire layout (zs/quantizer.py:133-149).
+
+        Wire scales are fp16; the tensor keeps them exactly as an f64 absmax of
+        ``scale16 * qmax`` (exact in f64), from which every kernel recovers
+        ``scale16`` bit-exactly (``RN64(scale16*qmax/qmax) == scale16``)."""
+        original_len, cfg, n_blocks, scale_end = from_bytes_header(raw)
+        scales16 = np.frombuffer(raw, dtype=np.float16, count=n_blocks, offset=_HEADER.size)
+        absmax = scales16.astype(np.float64) * cfg.qmax
+        codes = np.frombuffer(raw, dtype=np.uint8, offset=scale_end).copy()
+        dev = device()
+        return cls(codes=torch.from_numpy(codes).to(dev), absmax=torch.from_numpy(absmax).to(dev),
+                   original_len=original_len, config=cfg)
+
     def slice_blocks(self, start: int, length: int) -> "QuantizedTensor":
         """Elements [start, start+length) as a zero-copy view (zs/quantizer.py:151-169)."""
         bs = self.config.block_size

@@ -299,6 +299,25 @@ def build_collectives():
     print("collective cases:", {k: len(v) for k, v in meta.items()})
 
 
+def build_wire():
+    """to_bytes / from_bytes (zs/quantizer.py:121-149): raw wire bytes and the
+    values the reference decodes from them (fp16 wire scales)."""
+    out, meta = {}, []
+    rng = np.random.default_rng(5)
+    for i, (n, bits, block) in enumerate([(777, 4, 64), (5000, 8, 2048), (1021, 4, 512), (64, 8, 64)]):
+        q = zs.quantize(zs.FlatTensor(rng.normal(size=n) * 3), zs.QuantConfig(bit_width=bits, block_size=block))
+        raw = q.to_bytes()
+        back = zs.QuantizedTensor.from_bytes(raw)
+        out[f"{i}_raw"] = np.frombuffer(raw, dtype=np.uint8)
+        out[f"{i}_codes"] = q.codes
+        out[f"{i}_scales"] = q.scales
+        out[f"{i}_deq_from_bytes"] = zs.dequantize(back).values
+        meta.append(dict(idx=i, n=n, bits=bits, block=block))
+    out["meta"] = np.array(json.dumps(meta))
+    np.savez_compressed(os.path.join(HERE, "wire.npz"), **out)
+    print("wire cases:", len(meta))
+
+
 def build_volumes():
     """step_volumes CSV (ledger volume rows) for the ZeRO / ZeRO++ switches."""
     rows = []
@@ -321,3 +340,4 @@ if __name__ == "__main__":
     build_fused()
     build_collectives()
     build_volumes()
+    build_wire()

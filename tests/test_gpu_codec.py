@@ -284,3 +284,30 @@ def test_dequant16_fast_path_bit_exact_stress(src, bits, block):
         want = gu.round_to(ref, name)
         bad = np.flatnonzero(~((got == want) | (np.isnan(got) & np.isnan(want))))
         assert bad.size == 0, (name, bad[:5], got[bad[:5]], want[bad[:5]])
+
+
+def test_wire_format_roundtrip_golden():
+    """to_bytes / from_bytes (zs/quantizer.py:121-149): our bytes equal the
+    reference's, and decoding them gives the reference's values."""
+    zpp = _zpp()
+    z, meta = gu.load("wire")
+    for m in meta:
+        i = m["idx"]
+        cfg = zpp.QuantConfig(bit_width=m["bits"], block_size=m["block"])
+        raw = bytes(z[f"{i}_raw"].tobytes())
+        back = zpp.QuantizedTensor.from_bytes(raw)
+        assert back.original_len == m["n"] and back.config == cfg
+        assert np.array_equal(back.codes.cpu().numpy(), z[f"{i}_codes"])
+        assert np.array_equal(zpp.dequantize(back).values.cpu().numpy(), z[f"{i}_deq_from_bytes"])
+        assert back.to_bytes() == raw
+    with pytest.raises(zpp.IntegrityError):
+        zpp.QuantizedTensor.from_bytes(b"\x00\x01")
+    with pytest.raises(zpp.IntegrityError):
+        zpp.QuantizedTensor.from_bytes(raw[:-1])
+
+
+def test_serialization_is_deterministic():
+    zpp = _zpp()
+    x = torch.from_numpy(np.random.default_rng(5).normal(size=777)).cuda()
+    cfg = zpp.QuantConfig(bit_width=4, block_size=64)
+    assert zpp.quantize(x, cfg).to_bytes() == zpp.quantize(x, cfg).to_bytes()

@@ -236,3 +236,60 @@ def test_qgz_large_bucket_vs_oracle():
     want = O.qgz_2hop([gu.as_f64(b, "bf16") for b in bf], x, y, s, 4, 512)
     for r in range(world):
         assert np.array_equal(res.shards[r].values.cpu().numpy(), want[r])
+
+
+# --- comparators (pkg/tests/test_collectives.py:164-187, :230-249, :291-302) ---
+
+
+def test_naive_quant_ring_depth_and_volume():
+    zpp = _zpp()
+    topo = zpp.ClusterTopology(nodes=2, gpus_per_node=2)
+    ledger = zpp.TrafficLedger()
+    cfg = zpp.QuantConfig(bit_width=8, block_size=8)
+    ins = random_tensors(4, 32, seed=9, scale=2.0)
+    res = zpp.reduce_scatter_ring_naive_quant(ins, cfg, topo, ledger)
+    assert res.codec_depth == 3
+    oracle = O.reduce_scatter_ring([t.cpu().numpy() for t in ins], 4)
+    for got, want in zip(res.shards, oracle):
+        assert np.max(np.abs(got.values.cpu().numpy() - want)) < 1.0
+    assert ledger.volume_bytes(zpp.INTER, label="reduce_scatter") == 4 * 8
+    assert ledger.volume_bytes(zpp.INTER, label="reduce_scatter", kind="metadata") == 4 * 2
+    pt = zpp.reduce_scatter_ring_naive_quant(random_tensors(4, 16, seed=10, integers=True), zpp.PassthroughCodec(),
+                                             topo, zpp.TrafficLedger())
+    assert pt.codec_depth == 0
+
+
+def test_qgz_1hop_passthrough_and_volume():
+    zpp = _zpp()
+    topo = zpp.ClusterTopology(nodes=2, gpus_per_node=2)
+    ins = random_tensors(4, 16, seed=11, integers=True)
+    res = zpp.qgz_1hop(ins, zpp.PassthroughCodec(), topo, zpp.TrafficLedger())
+    oracle = O.reduce_scatter_ring([t.cpu().numpy() for t in ins], 4)
+    for got, want in zip(res.shards, oracle):
+        assert np.array_equal(got.values.cpu().numpy(), want)
+    ledger = zpp.TrafficLedger()
+    res = zpp.qgz_1hop(random_tensors(4, 32, seed=12), zpp.QuantConfig(bit_width=8, block_size=8), topo, ledger)
+    assert res.codec_depth == 1
+    assert ledger.volume_bytes(zpp.INTER, label="reduce_scatter") == 2 * 32
+    assert ledger.volume_bytes(zpp.INTER, label="reduce_scatter", kind="metadata") == 2 * 8
+
+
+def test_two_hop_beats_naive_ring_and_depth_is_two():
+    """Acceptance c05 (pkg/tests/test_acceptance.py:190-224)."""
+    zpp = _zpp()
+    cfg = zpp.QuantConfig(bit_width=4, block_size=8)
+    depths = {}
+    for nodes, gpus in ((2, 2), (4, 2), (4, 4)):
+        topo = zpp.ClusterTopology(nodes=nodes, gpus_per_node=gpus)
+        world = nodes * gpus
+        ins = random_tensors(world, world * 64, seed=50 + world, scale=2.0)
+        hier = zpp.qgz_2hop(ins, cfg, topo, zpp.TrafficLedger())
+        naive = zpp.reduce_scatter_ring_naive_quant(ins, cfg, topo, zpp.TrafficLedger())
+        assert hier.codec_depth == 2
+        depths[world] = naive.codec_depth
+        if world == 16:
+            oracle = O.reduce_scatter_ring([t.cpu().numpy() for t in ins], world)
+            rh = np.sqrt(np.mean([(g.values.cpu().numpy() - w) ** 2 for g, w in zip(hier.shards, oracle)]))
+            rn = np.sqrt(np.mean([(g.values.cpu().numpy() - w) ** 2 for g, w in zip(naive.shards, oracle)]))
+            assert rh < rn
+    assert depths == {4: 3, 8: 7, 16: 15}

@@ -121,3 +121,45 @@ def test_topology_and_ledger_basics():
     led.record_volume("x", zpp.INTER, payload=2 << 20)
     assert zpp.normalized_cross_node_volume(led, 1 << 20, label="x") == 1.0
     assert led.conservation_holds()
+
+
+def test_step_volumes_match_reference_ledger():
+    """Comm-only ZeRO/ZeRO++ step (zs/engine.py:455-506): the ledger CSV and the
+    normalised cross-node volumes equal the reference's for 15 switch settings."""
+    import paper_2306_10209_b200 as zpp
+
+    for row in gu.volumes():
+        cfg = zpp.StepConfig(nodes=row["nodes"], gpus_per_node=row["gpn"], quantized_weight_gather=row["qw"],
+                             hierarchical_secondary_gather=row["hp"], quantized_grad_reduce=row["qg"])
+        ledger, vols, traces = zpp.step_volumes(cfg, row["m"])
+        assert ledger.to_csv(row["m"]) == row["csv"], row
+        assert vols == row["vols"], row
+        assert ledger.conservation_holds()
+
+
+def test_step_volume_table_headline():
+    """Acceptance c01 (pkg/tests/test_acceptance.py:67-93): 8 nodes x 4 GPUs, 2^20
+    params: ZeRO-3 moves (1, 1, 1) fp16 model copies across nodes, ZeRO++ (0.5, 0,
+    0.25); scale metadata stays under 2% of payload."""
+    import paper_2306_10209_b200 as zpp
+
+    m = 1 << 20
+    _, base, _ = zpp.step_volumes(zpp.StepConfig(nodes=8, gpus_per_node=4), m)
+    led, comp, _ = zpp.step_volumes(zpp.StepConfig(nodes=8, gpus_per_node=4, quantized_weight_gather=True,
+                                                   hierarchical_secondary_gather=True,
+                                                   quantized_grad_reduce=True), m)
+    assert base == {zpp.FWD_GATHER: 1.0, zpp.BWD_GATHER: 1.0, zpp.GRAD_REDUCE: 1.0}
+    assert comp == {zpp.FWD_GATHER: 0.5, zpp.BWD_GATHER: 0.0, zpp.GRAD_REDUCE: 0.25}
+    assert max(b.metadata / b.payload for b in led.volume.values() if b.payload) < 0.02
+
+
+def test_secondary_gather_stays_on_node():
+    """Acceptance c07: hpZ's backward gather moves zero cross-node bytes."""
+    import paper_2306_10209_b200 as zpp
+
+    for nodes, gpus in ((2, 2), (2, 4), (3, 2), (4, 4)):
+        led, _, _ = zpp.step_volumes(zpp.StepConfig(nodes=nodes, gpus_per_node=gpus,
+                                                    hierarchical_secondary_gather=True), 1 << 16)
+        assert led.physical_bytes(label=zpp.BWD_GATHER, cls=zpp.INTER) == 0
+    off, _, _ = zpp.step_volumes(zpp.StepConfig(nodes=2, gpus_per_node=2), 1 << 16)
+    assert off.physical_bytes(label=zpp.BWD_GATHER, cls=zpp.INTER) > 0
