@@ -233,7 +233,8 @@ def run_ours(args):
         time.sleep(0.06)
     clk = clocks.stop() if rank == 0 else None
     comm.check()
-    launches_per_step = 2 + (1 if world > 1 else 0)  # quantize, [barrier], gather-dequantize
+    # N = 1: one fused quantize->dequantize kernel; N > 1: quantize, barrier, TMA gather
+    launches_per_step = 1 if world == 1 else 3
     value = world * 2 * M_PARAMS / t_step / 1e9
 
     # ---- per-kernel roofline (CUDA events around each kernel alone) ----------
@@ -266,18 +267,21 @@ def run_ours(args):
             "dequant16_kernel (gather)": {"us": kg * 1e6, "alg_bytes": g_alg, "GBps": g_alg / kg / 1e9}}
     traffic = ncu_traffic()
     if world == 1:
-        dom = "dequant16_kernel (gather)" if kg >= kq else "quantize_reg_kernel"
+        fused_alg = 4 * shard_len + qbytes  # read fp16, write codes + absmax, write fp16
+        kern["quantize_reg_kernel<deq> (fused qwZ self-gather)"] = {"us": t_step * 1e6, "alg_bytes": fused_alg,
+                                                                   "GBps": fused_alg / t_step / 1e9}
+        dom = "quantize_reg_kernel<deq> (fused qwZ self-gather)"
         d = kern[dom]
         roof = {"kernel": dom, "bound": "hbm", "achieved": d["GBps"], "peak": hbm_peak, "unit": "GB/s",
                 "frac": d["GBps"] / hbm_peak, "traffic": traffic.get(dom), "peak_kind": peak_kind,
-                "alg_bytes_per_launch": d["alg_bytes"], "launch_us": d["us"],
-                "kernels": kern}
+                "alg_bytes_per_launch": d["alg_bytes"], "launch_us": d["us"], "kernels": kern}
     else:
         ingress = (world - 1) * qbytes
         ach = ingress / kg / 1e9
-        roof = {"kernel": "dequant16_kernel (gather over NVLink)", "bound": "nvlink", "achieved": ach,
+        roof = {"kernel": "dequant16_tma_kernel (gather over NVLink)", "bound": "nvlink", "achieved": ach,
                 "peak": NVLINK_PEER_GBS, "unit": "GB/s", "frac": ach / NVLINK_PEER_GBS,
-                "traffic": traffic.get("dequant16_kernel (gather)"), "peak_kind": "measured peer copy, per direction",
+                "traffic": traffic.get("dequant16_tma_kernel (gather over NVLink)"),
+                "peak_kind": "measured peer copy, per direction",
                 "alg_bytes_per_launch": ingress, "launch_us": kg * 1e6, "kernels": kern,
                 "hbm": {"achieved": kern["dequant16_kernel (gather)"]["GBps"], "peak": hbm_peak,
                         "frac": kern["dequant16_kernel (gather)"]["GBps"] / hbm_peak}}

@@ -55,7 +55,7 @@ static int run_qreg(const T* x, const Addr& addr, int64_t n_blocks, uint8_t* cod
                     cudaStream_t st) {
   auto k = quantize_reg_kernel<T, BITS, LANES, EPL, Addr>;
   const int grid = grid_for(k, 256, ceil_div(n_blocks, 256 / LANES));
-  k<<<grid, 256, 0, st>>>(x, addr, n_blocks, codes, absmax, flag);
+  k<<<grid, 256, 0, st>>>(x, addr, n_blocks, codes, absmax, flag, nullptr);
   return check_cuda(cudaGetLastError(), "quantize_reg_kernel launch");
 }
 
@@ -125,6 +125,49 @@ static int quantize_dispatch(const void* x, int dtype, const Addr& addr, int64_t
   }
 #undef ZPP_Q
   return fail(ZPP_ERR_VALIDATION, "unknown input dtype");
+}
+
+// quantize + write dequantize(quantize(x)) in one pass (fp16/bf16 in = out,
+// register-path blocks, aligned).  Returns false when not applicable.
+template <typename T, int BITS>
+static bool qdeq_t(const T* x, int64_t n, int64_t block, uint8_t* codes, float* absmax, T* out, uint32_t* flag,
+                   cudaStream_t st, int* rc) {
+  constexpr int64_t EPL = Raw<T>::kEPL;
+  const int64_t nb = ceil_div(n, block);
+  PlainAddr addr{n, block};
+#define ZPP_QD(L)                                                                         \
+  {                                                                                       \
+    auto k = quantize_reg_kernel<T, BITS, L, (int)EPL, PlainAddr, true>;                  \
+    const int grid = grid_for(k, 256, ceil_div(nb, 256 / L));                             \
+    k<<<grid, 256, 0, st>>>(x, addr, nb, codes, absmax, flag, out);                       \
+    *rc = check_cuda(cudaGetLastError(), "quantize_reg_kernel<deq> launch");              \
+    return true;                                                                          \
+  }
+  if (block == 8 * EPL) ZPP_QD(8)
+  if (block == 16 * EPL) ZPP_QD(16)
+  if (block == 32 * EPL) ZPP_QD(32)
+#undef ZPP_QD
+  return false;
+}
+
+int launch_quantize_deq(const void* x, int dtype, int64_t n, int bits, int64_t block, uint8_t* codes, void* absmax,
+                        void* out, uint32_t* flag, cudaStream_t st, bool* handled) {
+  *handled = false;
+  if (n == 0 || !aligned16(x) || !aligned16(out) || n % 8 != 0) return ZPP_OK;
+  int rc = ZPP_OK;
+  float* am = reinterpret_cast<float*>(absmax);
+  if (dtype == ZPP_F16) {
+    auto xx = reinterpret_cast<const __half*>(x);
+    auto oo = reinterpret_cast<__half*>(out);
+    *handled = bits == 8 ? qdeq_t<__half, 8>(xx, n, block, codes, am, oo, flag, st, &rc)
+                         : qdeq_t<__half, 4>(xx, n, block, codes, am, oo, flag, st, &rc);
+  } else if (dtype == ZPP_BF16) {
+    auto xx = reinterpret_cast<const __nv_bfloat16*>(x);
+    auto oo = reinterpret_cast<__nv_bfloat16*>(out);
+    *handled = bits == 8 ? qdeq_t<__nv_bfloat16, 8>(xx, n, block, codes, am, oo, flag, st, &rc)
+                         : qdeq_t<__nv_bfloat16, 4>(xx, n, block, codes, am, oo, flag, st, &rc);
+  }
+  return rc;
 }
 
 int launch_quantize(const void* x, int dtype, const AddrSpec& a, int64_t n_out, int bits, int64_t block,

@@ -256,6 +256,13 @@ int zpp_qwz_allgather(zpp_comm_t c, size_t sym_offset, const void* shard, int dt
   uint32_t* flag = reinterpret_cast<uint32_t*>(errflag);
   const size_t base = sym_offset + (c->qwz_uses++ & 1) * region;
   const size_t abs_off = align256((size_t)code_bytes(shard_len, bits, block));
+  if (c->world == 1 && sec_out == nullptr && out_dtype == dtype) {
+    // 1-GPU world: the gather is the local round trip -- one fused pass
+    bool handled = false;
+    rc = launch_quantize_deq(shard, dtype, shard_len, bits, block, c->local + base, c->local + base + abs_off, out,
+                             flag, st, &handled);
+    if (rc || handled) return rc;
+  }
   AddrSpec a;
   a.n = shard_len;
   rc = launch_quantize(shard, dtype, a, shard_len, bits, block, c->local + base,

@@ -26,6 +26,8 @@ struct AddrSpec {
 // launchers (validated arguments)
 int launch_quantize(const void* x, int dtype, const AddrSpec& a, int64_t n_out, int bits, int64_t block,
                     uint8_t* codes, void* absmax, uint32_t* flag, cudaStream_t st);
+int launch_quantize_deq(const void* x, int dtype, int64_t n, int bits, int64_t block, uint8_t* codes, void* absmax,
+                        void* out, uint32_t* flag, cudaStream_t st, bool* handled);
 int launch_gather_dequant(const void* const* codes, const void* const* absmax, int absmax_dtype, int n_src,
                           int rot, int64_t shard_len, int bits, int64_t block, void* out, int out_dtype,
                           void* sec_out, int64_t sec_lo, int64_t sec_len, uint32_t* flag, cudaStream_t st,

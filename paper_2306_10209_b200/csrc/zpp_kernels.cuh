@@ -182,6 +182,34 @@ __device__ __forceinline__ void store_codes8(uint8_t* dst, const uint32_t (&b)[8
   }
 }
 
+// Fast 16-bit output of a unit: p = RN32(code * s32) with s32 = RN32(m * RN32(1/q))
+// is within 3 fp32 ulps of the exact f64 product code*s64, so RN16(p) equals
+// RN16(RN64(code*s64)) unless p lies within 64 ulps of a 16-bit rounding
+// midpoint; the unit is then redone in f64.  Out-of-range scales (16-bit
+// subnormal results, overflow) take the f64 path up front.
+template <typename O> struct Out16;
+template <> struct Out16<__half> {
+  // zero iff the 13 bits below the fp16 mantissa are within [-64, +64) of 0x1000
+  __device__ static uint32_t near_mid(uint32_t bits) { return ((bits + 0x40u) & 0x1F80u) ^ 0x1000u; }
+  __device__ static bool scale_ok(float s, int qmax) { return s >= 0x1p-14f && s * (float)qmax < 65504.0f; }
+  static constexpr uint32_t kLowMask = 0x1FFFu;  // absmax has <= 11 significant bits
+  __device__ static bool in_range(float m) { return m <= 65504.0f; }
+  __device__ static uint32_t pack2(float a, float b) {
+    __half2 h = __floats2half2_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+  }
+};
+template <> struct Out16<__nv_bfloat16> {
+  __device__ static uint32_t near_mid(uint32_t bits) { return ((bits + 0x40u) & 0xFF80u) ^ 0x8000u; }
+  __device__ static bool scale_ok(float s, int qmax) { return s >= 0x1p-125f && s * (float)qmax < 0x1p127f; }
+  static constexpr uint32_t kLowMask = 0xFFFFu;  // absmax has <= 8 significant bits
+  __device__ static bool in_range(float m) { return m >= 0x1p-100f && m < 0x1p127f; }
+  __device__ static uint32_t pack2(float a, float b) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+  }
+};
+
 // Quantize one chunk of 8 floats.  Fast path (fp32, packed):
 //   u = RN(x*inv32 + 1.5*2^23) = 1.5*2^23 + k with k = rint(x*inv32)  (FFMA2)
 //   e = RN(x*inv32 - k)                                                (FFMA2)
@@ -226,10 +254,15 @@ __device__ __forceinline__ void quant_chunk(const float (&v)[8], float inv32, do
 // chunks c*LANES + l, so each team-wide load covers one contiguous span of
 // >= 128 B.
 
-template <typename T, int BITS, int LANES, int EPL, typename Addr>
+// DEQ = true additionally writes dequantize(quantize(x)) to deq_out (same
+// 16-bit type as the input): the qwZ self-gather of a 1-GPU world in one pass
+// (5 instead of 6 bytes of HBM traffic per element).  For fp16/bf16 sources
+// the block absmax fits the output significand, so by the exact16 argument
+// (see decode16_any) the fp32 product rounds to the reference's value.
+template <typename T, int BITS, int LANES, int EPL, typename Addr, bool DEQ = false>
 __global__ void __launch_bounds__(256)
 quantize_reg_kernel(const T* __restrict__ x, Addr addr, int64_t n_blocks, uint8_t* __restrict__ codes,
-                    float* __restrict__ absmax, uint32_t* __restrict__ flag) {
+                    float* __restrict__ absmax, uint32_t* __restrict__ flag, T* __restrict__ deq_out = nullptr) {
   static_assert(32 % LANES == 0 && EPL % 8 == 0, "team shape");
   constexpr int B = LANES * EPL;
   constexpr int CH = EPL / 8;
@@ -294,6 +327,36 @@ quantize_reg_kernel(const T* __restrict__ x, Addr addr, int64_t n_blocks, uint8_
         for (int i = 0; i < 8; ++i) q[i] = q_exact<QMAX>((double)v[i], inv64);
       }
       if (active) store_codes8<BITS>(out + (c * LANES + tl) * BITS, q);
+      if constexpr (DEQ) {
+        if (active) {
+          // code as an exact float: the low byte of q is the two's complement code
+          const float s32 = __fmul_rn(m, 1.0f / QMAX);
+          const bool ok16 = Out16<T>::in_range(m);
+          uint32_t h[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const float c0 = (float)(int)(int8_t)(q[2 * i] & 0xFFu);
+            const float c1 = (float)(int)(int8_t)(q[2 * i + 1] & 0xFFu);
+            if (ok16) {
+              const float2 p = fmul2(make_float2(c0, c1), make_float2(s32, s32));
+              h[i] = Out16<T>::pack2(p.x, p.y);
+            } else {
+              const double s64 = scale_of<BITS>((double)m);
+              T a = from_f64<T>(__dmul_rn((double)c0, s64)), bb = from_f64<T>(__dmul_rn((double)c1, s64));
+              h[i] = (uint32_t)(*reinterpret_cast<uint16_t*>(&a)) | ((uint32_t)(*reinterpret_cast<uint16_t*>(&bb)) << 16);
+            }
+          }
+          const int e = (c * LANES + tl) * 8;
+          T* dst = deq_out + b * (int64_t)B + e;
+          if (e + 8 <= valid) {
+            *reinterpret_cast<uint4*>(dst) = make_uint4(h[0], h[1], h[2], h[3]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              if (e + i < valid) reinterpret_cast<uint16_t*>(dst)[i] = (uint16_t)(h[i / 2] >> (16 * (i & 1)));
+          }
+        }
+      }
     }
   }
 }
@@ -470,34 +533,6 @@ template <> struct Bias<4> {
 template <int BITS> __device__ __forceinline__ double code_f64(uint32_t fbits) {
   return __dsub_rn(__hiloint2double(0x43380000, (int)(fbits & 0xFFu)), Bias<BITS>::kD);
 }
-
-// Fast 16-bit output of a unit: p = RN32(code * s32) with s32 = RN32(m * RN32(1/q))
-// is within 3 fp32 ulps of the exact f64 product code*s64, so RN16(p) equals
-// RN16(RN64(code*s64)) unless p lies within 64 ulps of a 16-bit rounding
-// midpoint; the unit is then redone in f64.  Out-of-range scales (16-bit
-// subnormal results, overflow) take the f64 path up front.
-template <typename O> struct Out16;
-template <> struct Out16<__half> {
-  // zero iff the 13 bits below the fp16 mantissa are within [-64, +64) of 0x1000
-  __device__ static uint32_t near_mid(uint32_t bits) { return ((bits + 0x40u) & 0x1F80u) ^ 0x1000u; }
-  __device__ static bool scale_ok(float s, int qmax) { return s >= 0x1p-14f && s * (float)qmax < 65504.0f; }
-  static constexpr uint32_t kLowMask = 0x1FFFu;  // absmax has <= 11 significant bits
-  __device__ static bool in_range(float m) { return m <= 65504.0f; }
-  __device__ static uint32_t pack2(float a, float b) {
-    __half2 h = __floats2half2_rn(a, b);
-    return *reinterpret_cast<uint32_t*>(&h);
-  }
-};
-template <> struct Out16<__nv_bfloat16> {
-  __device__ static uint32_t near_mid(uint32_t bits) { return ((bits + 0x40u) & 0xFF80u) ^ 0x8000u; }
-  __device__ static bool scale_ok(float s, int qmax) { return s >= 0x1p-125f && s * (float)qmax < 0x1p127f; }
-  static constexpr uint32_t kLowMask = 0xFFFFu;  // absmax has <= 8 significant bits
-  __device__ static bool in_range(float m) { return m >= 0x1p-100f && m < 0x1p127f; }
-  __device__ static uint32_t pack2(float a, float b) {
-    __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
-    return *reinterpret_cast<uint32_t*>(&h);
-  }
-};
 
 template <typename O>
 __device__ __forceinline__ void store_scalar(O* dst, int i, uint32_t bits16) {

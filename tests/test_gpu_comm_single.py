@@ -46,3 +46,25 @@ def test_world1_collectives():
     with pytest.raises(zpp.ValidationError):
         comm.qwz_allgather(torch.zeros(n + 8, device="cuda", dtype=torch.float16))
     comm.close()
+
+
+@pytest.mark.parametrize("dtype,bits,block", [("fp16", 8, 2048), ("bf16", 8, 2048), ("fp16", 4, 512),
+                                              ("bf16", 4, 1024)])
+def test_world1_fused_round_trip(dtype, bits, block):
+    """1-GPU qwZ takes the fused quantize->dequantize pass (codes still land in
+    the symmetric buffer); output = the reference's value rounded once."""
+    import paper_2306_10209_b200 as zpp
+    from paper_2306_10209_b200.dist import Communicator
+
+    n = 37 * block + 776  # partial last block, n % 8 == 0
+    rng = np.random.default_rng(bits * block)
+    v = rng.normal(size=n) * np.exp(rng.normal(size=n) * 2) * 0.02
+    arr = v.astype(np.float16) if dtype == "fp16" else (v.astype(np.float32).view(np.uint32) >> 16).astype(np.uint16)
+    x = gu.to_torch(arr, dtype)
+    comm = Communicator(qwz_shard=n, qwz_cfg=zpp.QuantConfig(bit_width=bits, block_size=block))
+    out = comm.qwz_allgather(x, out_dtype=x.dtype)
+    comm.check()
+    want, _ = O.all_gather_qwz([gu.as_f64(arr, dtype)], bits, block)
+    got = out.to(torch.float64).cpu().numpy()
+    assert np.array_equal(got, gu.round_to(want, dtype))
+    comm.close()

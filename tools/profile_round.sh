@@ -10,7 +10,7 @@ OUT=gpurun_out
 python bench.py --steps 2 --warmup 3 > $OUT/plain_$R.log 2>&1 || { echo "plain bench failed"; exit 1; }
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $OUT/ncu_launches_$R.csv \
     python bench.py --steps 2 --warmup 3 > $OUT/ncu_launches_$R.log 2>&1
-for K in quantize_reg_kernel dequant16_kernel drq16_kernel dequant_reduce16_kernel; do
+for K in quantize_reg_kernel dequant_reduce16_kernel drq16_kernel; do
   ncu --set full --clock-control none --import-source on -k regex:"${K}" -s 2 -c 1 -o /tmp/prof_$K \
       python bench.py --steps 2 --warmup 3 > $OUT/ncu_full_${R}_$K.log 2>&1
   ncu -i /tmp/prof_$K.ncu-rep --page details --csv > $OUT/ncu_full_${R}_$K.csv 2>/dev/null
@@ -19,7 +19,7 @@ done
 python - <<'EOF'
 import csv, json, glob, os
 out = {}
-names = {"quantize_reg_kernel": "quantize_reg_kernel", "dequant16_kernel": "dequant16_kernel (gather)",
+names = {"quantize_reg_kernel": "quantize_reg_kernel<deq> (fused qwZ self-gather)",
          "drq16_kernel": "drq16_kernel", "dequant_reduce16_kernel": "dequant_reduce16_kernel"}
 for f in glob.glob("/tmp/raw_*.csv"):
     k = os.path.basename(f)[4:-4]
