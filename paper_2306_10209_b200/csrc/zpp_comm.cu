@@ -85,6 +85,59 @@ gather_copy_kernel(SrcTable src, int n_src, int rot, int64_t seg_bytes, uint8_t*
   }
 }
 
+// TMA-pipelined peer copy (hpZ gather): one elected thread streams 8 KB tiles
+// of each group member's secondary shard into a 4-deep shared ring with
+// cp.async.bulk; all threads write them out with 16-byte stores.
+constexpr int kCopyStages = 4;
+constexpr int kCopyTile = 8192;  // bytes
+
+__global__ void __launch_bounds__(256)
+gather_copy_tma_kernel(SrcTable src, int n_src, int rot, int64_t seg_bytes, uint8_t* __restrict__ out) {
+  extern __shared__ __align__(128) uint8_t dsm[];
+  uint8_t* ring = dsm;
+  uint64_t* full = reinterpret_cast<uint64_t*>(dsm + kCopyStages * kCopyTile);
+  const int tid = threadIdx.x;
+  const int tiles = (int)((seg_bytes + kCopyTile - 1) / kCopyTile);
+  const int n_tiles = tiles * n_src;
+  if (tid == 0) {
+    for (int i = 0; i < kCopyStages; ++i) mbar_init(&full[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto locate = [&](int g, int& s, int& t) {
+    t = g / n_src;
+    s = g - t * n_src + rot;
+    if (s >= n_src) s -= n_src;
+  };
+  auto issue = [&](int g, int slot) {
+    if (g < n_tiles) {
+      int s, t;
+      locate(g, s, t);
+      const int64_t off = (int64_t)t * kCopyTile;
+      const uint32_t bytes = (uint32_t)min((int64_t)kCopyTile, seg_bytes - off);
+      mbar_expect_tx(&full[slot], bytes);
+      bulk_g2s(ring + slot * kCopyTile, src.codes[s] + off, bytes, &full[slot]);
+    }
+  };
+  const int G = gridDim.x;
+  if (tid == 0)
+    for (int k = 0; k < kCopyStages - 1; ++k) issue(blockIdx.x + k * G, k);
+  int k = 0;
+  for (int g = blockIdx.x; g < n_tiles; g += G, ++k) {
+    const int slot = k % kCopyStages;
+    if (tid == 0) issue(g + (kCopyStages - 1) * G, (k + kCopyStages - 1) % kCopyStages);
+    mbar_wait(&full[slot], (uint32_t)((k / kCopyStages) & 1));
+    int s, t;
+    locate(g, s, t);
+    const int64_t off = (int64_t)t * kCopyTile;
+    const int bytes = (int)min((int64_t)kCopyTile, seg_bytes - off);
+    uint8_t* dst = out + s * seg_bytes + off;
+    const uint4* sm = reinterpret_cast<const uint4*>(ring + slot * kCopyTile);
+    for (int i = tid; i < bytes / 16; i += 256) reinterpret_cast<uint4*>(dst)[i] = sm[i];
+    __syncthreads();
+  }
+}
+
 }  // namespace
 
 struct zpp_comm {
@@ -302,6 +355,16 @@ int zpp_hpz_allgather(zpp_comm_t c, size_t sym_offset, int64_t sec_len, int elem
   for (size_t i = 0; i < m.size(); ++i) t.codes[i] = c->peers[m[i]] + sym_offset;
   const int vec = (seg % 16 == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0) && (sym_offset % 16 == 0);
   const int n = (int)m.size();
+  if (vec) {
+    const int smem = kCopyStages * kCopyTile + kCopyStages * 8;
+    cudaFuncSetAttribute(gather_copy_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gather_copy_tma_kernel, 256, smem);
+    const int64_t tiles = ceil_div(seg, kCopyTile) * n;
+    const int grid = (int)std::min<int64_t>((int64_t)sm_count() * std::max(occ, 1), tiles);
+    gather_copy_tma_kernel<<<grid, 256, smem, st>>>(t, n, c->rank % c->group, seg, reinterpret_cast<uint8_t*>(out));
+    return check_cuda(cudaGetLastError(), "gather_copy_tma_kernel launch");
+  }
   const int grid = (int)std::min<int64_t>(4 * sm_count(), std::max<int64_t>(1, ceil_div(seg * n, 16 * 256)));
   gather_copy_kernel<<<grid, 256, 0, st>>>(t, n, c->rank % c->group, seg, reinterpret_cast<uint8_t*>(out), vec);
   return check_cuda(cudaGetLastError(), "gather_copy_kernel launch");
@@ -422,6 +485,14 @@ int zpp_qgz_reduce_scatter(zpp_comm_t c, size_t sym_offset, const void* grad, in
       const uint8_t* p = c->peers[node * X + j] + base;
       codes[j] = p + l.send_codes + (size_t)code_bytes(msg_elems, intra_bits, intra_block) * loc;
       absmax[j] = p + l.send_abs + (size_t)(msg_elems / intra_block) * in_abs_sz * loc;
+    }
+    if (Y == 1) {  // hop 2 is a self-send: K2 writes the final partition directly
+      bool handled = false;
+      rc = launch_drq_final(codes, absmax, in_abs, X, msg_elems, intra_bits, intra_block, inter_bits, inter_block,
+                            reinterpret_cast<double*>(c->local + base + l.hop_abs),
+                            reinterpret_cast<uint8_t*>(out) + (size_t)s * L * out_esz, out_dtype, flag, st, &handled);
+      if (rc) return rc;
+      if (handled) continue;
     }
     rc = launch_drq(codes, absmax, in_abs, X, msg_elems, intra_bits, intra_block, inter_bits, inter_block,
                     c->local + base + l.hop_codes, reinterpret_cast<double*>(c->local + base + l.hop_abs),

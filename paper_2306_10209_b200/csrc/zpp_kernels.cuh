@@ -882,9 +882,13 @@ dequant16_tma_kernel(SrcTable src, int n_src, int rot, int64_t shard_len, int64_
       }
       if (sec_out != nullptr && oi + cnt > sec_lo && oi < sec_lo + sec_len) {
         const int64_t k0 = oi - sec_lo;
+        if (vec_ok && cnt == E && k0 >= 0 && k0 + E <= sec_len) {
+          store_words<E / 2>(sec_out + k0, h);
+        } else {
 #pragma unroll
-        for (int i = 0; i < E; ++i)
-          if (i < cnt && k0 + i >= 0 && k0 + i < sec_len) store_scalar<O>(sec_out + k0, i, h[i / 2] >> (16 * (i & 1)));
+          for (int i = 0; i < E; ++i)
+            if (i < cnt && k0 + i >= 0 && k0 + i < sec_len) store_scalar<O>(sec_out + k0, i, h[i / 2] >> (16 * (i & 1)));
+        }
       }
     }
     __syncthreads();  // every thread is done with this slot before it is refilled
@@ -1276,10 +1280,14 @@ dequant_reduce16_kernel(SrcTable src, int n_src, int64_t n, int64_t B, O* __rest
 // elements, lane = 16 contiguous elements; sources folded in order (loads of
 // up to 4 in flight); requantized from the exact f64 block absmax (stored in
 // f64).  Requires n % 16 == 0, input block % 16 == 0, aligned code pointers.
-template <int IBITS, typename IA, int OBITS, int LANES, bool VALIDATE>
+//
+// FO != void (qgZ with a single group, Y = 1): hop 2 is a self-send, so instead
+// of storing the requantized codes the kernel emits what K3 would compute from
+// them -- fold(+0.0, code * RN64(absmax/qmax)) rounded once to FO.
+template <int IBITS, typename IA, int OBITS, int LANES, bool VALIDATE, typename FO = void>
 __global__ void __launch_bounds__(256)
 drq16_kernel(SrcTable src, int n_src, int64_t n, int64_t B1, int64_t n_blocks_out, uint8_t* __restrict__ codes,
-             double* __restrict__ absmax, uint32_t* __restrict__ flag) {
+             double* __restrict__ absmax, uint32_t* __restrict__ flag, FO* __restrict__ final_out = nullptr) {
   using V = typename Vec16<IBITS>::T;
   constexpr int B2 = LANES * 16;
   constexpr int TPW = 32 / LANES;
@@ -1337,14 +1345,34 @@ drq16_kernel(SrcTable src, int n_src, int64_t n, int64_t B1, int64_t n_blocks_ou
         q0[i] = (uint32_t)rint_f64(__dmul_rn(acc[i], inv));
         q1[i] = (uint32_t)rint_f64(__dmul_rn(acc[8 + i], inv));
       }
-      uint8_t* dst = codes + u * 2 * OBITS;
-      if constexpr (OBITS == 8) {
-        const uint2 a = pack8_int8(q0), c = pack8_int8(q1);
-        *reinterpret_cast<uint4*>(dst) = make_uint4(a.x, a.y, c.x, c.y);
+      if constexpr (std::is_void<FO>::value) {
+        uint8_t* dst = codes + u * 2 * OBITS;
+        if constexpr (OBITS == 8) {
+          const uint2 a = pack8_int8(q0), c = pack8_int8(q1);
+          *reinterpret_cast<uint4*>(dst) = make_uint4(a.x, a.y, c.x, c.y);
+        } else {
+          *reinterpret_cast<uint2*>(dst) = make_uint2(pack8_int4(q0), pack8_int4(q1));
+        }
       } else {
-        *reinterpret_cast<uint2*>(dst) = make_uint2(pack8_int4(q0), pack8_int4(q1));
+        const double s2 = scale_of<OBITS>(mx);
+        double v[16];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          v[i] = __dadd_rn(0.0, __dmul_rn((double)(int)q0[i], s2));
+          v[8 + i] = __dadd_rn(0.0, __dmul_rn((double)(int)q1[i], s2));
+        }
+        FO* dst = final_out + e0;
+        if constexpr (sizeof(FO) == 4) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            reinterpret_cast<float4*>(dst)[i] = make_float4(from_f64<float>(v[4 * i]), from_f64<float>(v[4 * i + 1]),
+                                                            from_f64<float>(v[4 * i + 2]), from_f64<float>(v[4 * i + 3]));
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) reinterpret_cast<double2*>(dst)[i] = make_double2(v[2 * i], v[2 * i + 1]);
+        }
       }
-    } else if (b < n_blocks_out) {
+    } else if (b < n_blocks_out && std::is_void<FO>::value) {
       // zero padding of a partial last block (zs/quantizer.py:215-217)
       uint8_t* dst = codes + u * 2 * OBITS;
       if constexpr (OBITS == 8) *reinterpret_cast<uint4*>(dst) = make_uint4(0, 0, 0, 0);

@@ -63,7 +63,7 @@ static int run_drq(const SrcTable& t, int n_src, int64_t n, int64_t in_block, in
   if (n % 16 == 0 && in_block % 16 == 0 && codes_aligned(t, n_src, IBITS)) {
     auto k = validate ? drq16_kernel<IBITS, IA, OBITS, LANES, true> : drq16_kernel<IBITS, IA, OBITS, LANES, false>;
     const int grid = grid_for(k, 256, ceil_div(nbo, 256 / LANES));
-    k<<<grid, 256, 0, st>>>(t, n_src, n, in_block, nbo, codes, absmax, flag);
+    k<<<grid, 256, 0, st>>>(t, n_src, n, in_block, nbo, codes, absmax, flag, nullptr);
     return check_cuda(cudaGetLastError(), "drq16_kernel launch");
   }
   auto k = drq_reg_kernel<IBITS, IA, OBITS, LANES>;
@@ -124,6 +124,45 @@ int launch_drq(const void* const* codes, const void* const* absmax, int absmax_d
   AddrSpec a;
   a.n = n;
   return launch_quantize(workspace, ZPP_F64, a, n, out_bits, out_block, out_codes, out_absmax, flag, st);
+}
+
+// K2 whose hop-2 destination is itself (Y = 1): writes the final dequantized
+// partition instead of codes.  Fast-path shapes only (16-element lanes,
+// 512-element output blocks, validate off -- internal qgZ use).
+int launch_drq_final(const void* const* codes, const void* const* absmax, int absmax_dtype, int n_src, int64_t n,
+                     int in_bits, int64_t in_block, int out_bits, int64_t out_block, double* out_absmax, void* out,
+                     int out_dtype, uint32_t* flag, cudaStream_t st, bool* handled) {
+  *handled = false;
+  if (n == 0 || out_block != 512 || n % 16 || in_block % 16 || !aligned16(out)) return ZPP_OK;
+  if (out_dtype != ZPP_F32 && out_dtype != ZPP_F64) return ZPP_OK;
+  SrcTable t;
+  int rc = fill_table(t, codes, absmax, n_src);
+  if (rc) return rc;
+  if (!codes_aligned(t, n_src, in_bits)) return ZPP_OK;
+  if (absmax_dtype != ZPP_F32 && absmax_dtype != ZPP_F64) return ZPP_OK;
+  const int64_t nbo = ceil_div(n, out_block);
+  const bool a64 = absmax_dtype == ZPP_F64;
+#define ZPP_F(IB, IA, OB, FO)                                                                         \
+  {                                                                                                   \
+    auto k = drq16_kernel<IB, IA, OB, 32, false, FO>;                                                 \
+    const int grid = grid_for(k, 256, ceil_div(nbo, 8));                                              \
+    k<<<grid, 256, 0, st>>>(t, n_src, n, in_block, nbo, nullptr, out_absmax, flag,                    \
+                            reinterpret_cast<FO*>(out));                                              \
+    *handled = true;                                                                                  \
+    return check_cuda(cudaGetLastError(), "drq16_kernel<final> launch");                              \
+  }
+#define ZPP_FO(IB, IA, OB) \
+  if (out_dtype == ZPP_F32) ZPP_F(IB, IA, OB, float) else ZPP_F(IB, IA, OB, double)
+#define ZPP_FA(IB, OB) \
+  if (a64) { ZPP_FO(IB, double, OB) } else { ZPP_FO(IB, float, OB) }
+  if (in_bits == 4 && out_bits == 4) { ZPP_FA(4, 4) }
+  if (in_bits == 8 && out_bits == 4) { ZPP_FA(8, 4) }
+  if (in_bits == 4 && out_bits == 8) { ZPP_FA(4, 8) }
+  if (in_bits == 8 && out_bits == 8) { ZPP_FA(8, 8) }
+#undef ZPP_FA
+#undef ZPP_FO
+#undef ZPP_F
+  return ZPP_OK;
 }
 
 }  // namespace zpp

@@ -103,6 +103,9 @@ def main():
         comm.qgz_reduce_scatter(gl, out=gout)                     # gradient reduce
 
     t_zpp = timed(zeropp_layer, steps=10)
+    t_qwz = timed(lambda: comm.qwz_allgather(w, out=wout, write_secondary=True), steps=10)
+    t_hpz = timed(lambda: comm.hpz_allgather(out=wout), steps=10)
+    t_qgz = timed(lambda: comm.qgz_reduce_scatter(gl, out=gout), steps=10)
     comm.check()
     comm.close()
     bout = torch.empty(layer_p // world, dtype=torch.bfloat16, device=dev)
@@ -113,8 +116,10 @@ def main():
         nccl_reduce_scatter(gl, out=bout)
 
     t_z3 = timed(zero3_layer, steps=10)
-    res["gpt13b_layer_step_comm"] = {"layer_params": layer, "padded": layer_p, "zeropp_ms": t_zpp,
-                                     "zero3_nccl_ms": t_z3, "speedup": t_z3 / t_zpp,
+    t_ag = timed(lambda: nccl_allgather(w, out=wout), steps=10)
+    t_rs = timed(lambda: nccl_reduce_scatter(gl, out=bout), steps=10)
+    res["gpt13b_layer_step_comm"] = {"layer_params": layer, "padded": layer_p, "zeropp_ms": t_zpp, "parts_ms": {"qwz": t_qwz, "hpz": t_hpz, "qgz": t_qgz},
+                                     "zero3_nccl_ms": t_z3, "zero3_parts_ms": {"ag": t_ag, "rs": t_rs}, "speedup": t_z3 / t_zpp,
                                      "zeropp_40_layers_ms": 40 * t_zpp, "zero3_40_layers_ms": 40 * t_z3}
     if rank == 0:
         print(json.dumps(res), flush=True)
