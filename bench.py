@@ -31,6 +31,7 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+os.environ.setdefault("NCCL_DEBUG", "WARN")  # keep stdout to the one JSON line
 
 METRIC = "qwZ/qgZ effective GB/s at 1/2/4/8 B200; quant kernel HBM GB/s vs 8 TB/s"
 M_PARAMS = 1_300_004_864           # 1.3e9 rounded up to a multiple of 8 * 2048
@@ -59,13 +60,23 @@ def ncu_traffic():
 class ClockSampler:
     """nvidia-smi clocks/throttle reasons sampled during the timed region."""
 
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+    FIELDS = ("pci.bus_id,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
 
-    def __init__(self):
+    def __init__(self, pci=None):
         self.proc = None
         self.lines = []
+        self.pci = pci  # {(domain, bus, device)} of the job's GPUs; None = all
+
+    def _ours(self, bus_id: str) -> bool:
+        if self.pci is None:
+            return True
+        try:
+            dom, bus, devfn = bus_id.split(":")
+            return (int(dom, 16), int(bus, 16), int(devfn.split(".")[0], 16)) in self.pci
+        except ValueError:
+            return False
 
     def start(self):
         try:
@@ -94,15 +105,19 @@ class ClockSampler:
             self.proc.wait(timeout=5)
         except Exception:
             self.proc.kill()
-        sm, smax, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         lo, hi = getattr(self, "t_load", 0.0), getattr(self, "t_end", 1e30)
+        rows = []
         for ts, ln in self.lines:
-            if not lo <= ts <= hi:
-                continue  # only samples taken while the step was running
             parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 8:
-                continue
+            if lo <= ts <= hi and len(parts) >= 8:  # only samples taken while the step was running
+                rows.append(parts)
+        ours = [r for r in rows if self._ours(r[0])]
+        which = "the job's GPUs (matched by PCI bus id)"
+        if not ours:
+            ours, which = rows, "all GPUs (no PCI bus id match)"
+        sm, smax, reasons = [], [], set()
+        for parts in ours:
             try:
                 sm.append(float(parts[1]))
                 smax.append(float(parts[2]))
@@ -112,7 +127,7 @@ class ClockSampler:
                 if v.lower() == "active":
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "gpus": which}
 
 
 def cpu_reference(sample_elems: int, steps: int, warmup: int, threads: int):
@@ -213,7 +228,14 @@ def run_ours(args):
 
     # ---- headline: fused qwZ all-gather -----------------------------------
     step = lambda: comm.qwz_allgather(shard, out=out)
-    clocks = ClockSampler()
+    p = torch.cuda.get_device_properties(dev)
+    mine = (p.pci_domain_id, p.pci_bus_id, p.pci_device_id)
+    pci = [None] * world
+    if world > 1:
+        dist.all_gather_object(pci, mine)
+    else:
+        pci = [mine]
+    clocks = ClockSampler(set(pci))  # samples of the job's GPUs only
     if rank == 0:
         clocks.start()  # sampling spans warmup + the timed region
     for _ in range(args.warmup):

@@ -18,6 +18,7 @@
 
 #include "zpp_internal.h"
 #include "zpp_kernels.cuh"
+#include "zpp_launch.cuh"
 
 using namespace zpp;
 
@@ -148,6 +149,7 @@ struct zpp_comm {
   bool opened[kMaxRanks] = {};
   uint32_t epoch[kScopes] = {};
   uint64_t qwz_uses = 0, qgz_uses = 0;
+  size_t qgz_region = 0;  // region size of the last qgZ call
   cudaIpcMemHandle_t handle;
   int device = 0;
   // qgZ stage pipelining: K1 of stage s+1 runs on `side` while K2/K3 of stage
@@ -437,11 +439,24 @@ int zpp_qgz_reduce_scatter(zpp_comm_t c, size_t sym_offset, const void* grad, in
     if (!rc) rc = check_cuda(cudaEventCreateWithFlags(&c->ev_bar, cudaEventDisableTiming), "event");
     if (rc) return rc;
   }
+  // a different region size (another n or config) moves the half boundaries:
+  // drain every rank's reads of the previous layout first
+  if (c->qgz_region != 0 && c->qgz_region != l.region) {
+    if ((rc = barrier(c, 0, kBarrierTimeoutMs, flag, st))) return rc;
+  }
+  c->qgz_region = l.region;
   const uint64_t use0 = c->qgz_uses;
   c->qgz_uses += stages;
   auto base_of = [&](int s) { return sym_offset + ((use0 + s) & 1) * l.region; };
   // K1: swizzle + quantize stage s's slices into my send buffer [j][c][e]
+  // SM split while K1(s+1) runs beside K2(s) (pipelined only)
+  static const int k1_sms_env = [] {
+    const char* e = getenv("ZPP_QGZ_K1_SMS");
+    return e ? atoi(e) : 0;
+  }();
+  const int k1_sms = pipelined ? (k1_sms_env > 0 ? k1_sms_env : sm_count() / 3) : 0;
   auto k1 = [&](int s, cudaStream_t on) {
+    SmBudget budget(s > 0 ? k1_sms : 0);  // K1(0) runs alone
     AddrSpec a;
     a.swizzle = true;
     a.L = L;
@@ -478,6 +493,7 @@ int zpp_qgz_reduce_scatter(zpp_comm_t c, size_t sym_offset, const void* grad, in
       if ((rc = k1(s + 1, c->side))) return rc;
       if ((rc = check_cuda(cudaEventRecord(c->ev_k1, c->side), "record"))) return rc;
     }
+    SmBudget budget(pipelined && s + 1 < stages ? sm_count() - k1_sms : 0);
     // K2: pull message `loc` from every group member (ascending local rank)
     const void* codes[kMaxRanks];
     const void* absmax[kMaxRanks];

@@ -27,6 +27,8 @@ constexpr int kMaxSrc = 64;
 struct SrcTable {
   const uint8_t* codes[kMaxSrc];
   const void* absmax[kMaxSrc];
+  __device__ __forceinline__ const uint8_t* code_ptr(int s) const { return codes[s]; }
+  __device__ __forceinline__ const void* abs_ptr(int s) const { return absmax[s]; }
 };
 
 // ---------------------------------------------------------------------------
@@ -259,105 +261,112 @@ __device__ __forceinline__ void quant_chunk(const float (&v)[8], float inv32, do
 // (5 instead of 6 bytes of HBM traffic per element).  For fp16/bf16 sources
 // the block absmax fits the output significand, so by the exact16 argument
 // (see decode16_any) the fp32 product rounds to the reference's value.
+// One team of LANES lanes quantizes output block b (EPL elements per lane).
+// Shared by the K0/K1 grid-stride kernel and the fused qgZ kernel.
+template <typename T, int BITS, int LANES, int EPL, typename Addr, bool DEQ>
+__device__ __forceinline__ void quant_team(const T* __restrict__ x, const Addr& addr, int64_t b, bool active, int tl,
+                                           uint8_t* __restrict__ codes, float* __restrict__ absmax,
+                                           uint32_t* __restrict__ flag, T* __restrict__ deq_out) {
+  constexpr int B = LANES * EPL;
+  constexpr int CH = EPL / 8;
+  constexpr int RW = Raw<T>::W;
+  constexpr int QMAX = Codes<BITS>::kQmax;
+  int64_t src = 0, valid = 0;
+  if (active) {
+    src = addr.block_src(b);
+    valid = addr.valid(b * B);
+  }
+  uint32_t raw[CH][RW];
+  uint32_t acc = 0;
+  if (active && valid >= B) {  // full block: unconditional vector loads
+    const T* xb = x + src + tl * 8;
+#pragma unroll
+    for (int c = 0; c < CH; ++c) Raw<T>::load(xb + c * LANES * 8, raw[c]);
+  } else {
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      const int e = (c * LANES + tl) * 8;
+      if (active && e + 8 <= valid) {
+        Raw<T>::load(x + src + e, raw[c]);
+      } else {
+        const int cnt = active ? (int)max((int64_t)0, min((int64_t)8, valid - e)) : 0;
+        Raw<T>::load_scalar(x + src + e, cnt, raw[c]);
+      }
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < CH; ++c) acc = Raw<T>::absacc(raw[c], acc);
+  uint32_t mb = Raw<T>::finish(acc);
+#pragma unroll
+  for (int off = LANES / 2; off >= 1; off >>= 1) mb = max(mb, __shfl_xor_sync(0xffffffffu, mb, off));
+  const float m = Raw<T>::m_to_float(mb);
+  if (active && tl == 0) {
+    absmax[b] = m;
+    if (Raw<T>::nonfinite(mb)) raise_flag(flag, FLAG_NONFINITE);
+  }
+  const float inv32 = m > 0.0f ? __fdiv_rn((float)QMAX, m) : 0.0f;
+  const bool slow = !(inv32 <= 0x1p100f);  // reciprocal of a (sub)normal tiny absmax
+  const double inv64 = m > 0.0f ? __ddiv_rn((double)QMAX, (double)m) : 0.0;
+  uint8_t* out = codes + b * (int64_t)(B * BITS / 8);
+#pragma unroll
+  for (int c = 0; c < CH; ++c) {
+    float v[8];
+    uint32_t q[8];
+    Raw<T>::to_float(raw[c], v);
+    if (!slow) {
+      quant_chunk<QMAX>(v, inv32, inv64, q);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) q[i] = q_exact<QMAX>((double)v[i], inv64);
+    }
+    if (active) store_codes8<BITS>(out + (c * LANES + tl) * BITS, q);
+    if constexpr (DEQ) {
+      if (active) {
+        // code as an exact float: the low byte of q is the two's complement code
+        const float s32 = __fmul_rn(m, 1.0f / QMAX);
+        const bool ok16 = Out16<T>::in_range(m);
+        uint32_t h[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float c0 = (float)(int)(int8_t)(q[2 * i] & 0xFFu);
+          const float c1 = (float)(int)(int8_t)(q[2 * i + 1] & 0xFFu);
+          if (ok16) {
+            const float2 p = fmul2(make_float2(c0, c1), make_float2(s32, s32));
+            h[i] = Out16<T>::pack2(p.x, p.y);
+          } else {
+            const double s64 = scale_of<BITS>((double)m);
+            T a = from_f64<T>(__dmul_rn((double)c0, s64)), bb = from_f64<T>(__dmul_rn((double)c1, s64));
+            h[i] = (uint32_t)(*reinterpret_cast<uint16_t*>(&a)) | ((uint32_t)(*reinterpret_cast<uint16_t*>(&bb)) << 16);
+          }
+        }
+        const int e = (c * LANES + tl) * 8;
+        T* dst = deq_out + b * (int64_t)B + e;
+        if (e + 8 <= valid) {
+          *reinterpret_cast<uint4*>(dst) = make_uint4(h[0], h[1], h[2], h[3]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            if (e + i < valid) reinterpret_cast<uint16_t*>(dst)[i] = (uint16_t)(h[i / 2] >> (16 * (i & 1)));
+        }
+      }
+    }
+  }
+}
+
 template <typename T, int BITS, int LANES, int EPL, typename Addr, bool DEQ = false>
 __global__ void __launch_bounds__(256)
 quantize_reg_kernel(const T* __restrict__ x, Addr addr, int64_t n_blocks, uint8_t* __restrict__ codes,
                     float* __restrict__ absmax, uint32_t* __restrict__ flag, T* __restrict__ deq_out = nullptr) {
   static_assert(32 % LANES == 0 && EPL % 8 == 0, "team shape");
-  constexpr int B = LANES * EPL;
-  constexpr int CH = EPL / 8;
-  constexpr int RW = Raw<T>::W;
-  constexpr int QMAX = Codes<BITS>::kQmax;
   constexpr int TPW = 32 / LANES;
   const int lane = threadIdx.x & 31;
   const int tl = lane % LANES;
   const int team = lane / LANES;
   const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarp = ((int64_t)gridDim.x * blockDim.x) >> 5;
-
   for (int64_t wb = gwarp * TPW; wb < n_blocks; wb += nwarp * TPW) {
     const int64_t b = wb + team;
-    const bool active = b < n_blocks;
-    int64_t src = 0, valid = 0;
-    if (active) {
-      src = addr.block_src(b);
-      valid = addr.valid(b * B);
-    }
-    uint32_t raw[CH][RW];
-    uint32_t acc = 0;
-    if (active && valid >= B) {  // full block: unconditional vector loads
-      const T* xb = x + src + tl * 8;
-#pragma unroll
-      for (int c = 0; c < CH; ++c) Raw<T>::load(xb + c * LANES * 8, raw[c]);
-    } else {
-#pragma unroll
-      for (int c = 0; c < CH; ++c) {
-        const int e = (c * LANES + tl) * 8;
-        if (active && e + 8 <= valid) {
-          Raw<T>::load(x + src + e, raw[c]);
-        } else {
-          const int cnt = active ? (int)max((int64_t)0, min((int64_t)8, valid - e)) : 0;
-          Raw<T>::load_scalar(x + src + e, cnt, raw[c]);
-        }
-      }
-    }
-#pragma unroll
-    for (int c = 0; c < CH; ++c) acc = Raw<T>::absacc(raw[c], acc);
-    uint32_t mb = Raw<T>::finish(acc);
-#pragma unroll
-    for (int off = LANES / 2; off >= 1; off >>= 1) mb = max(mb, __shfl_xor_sync(0xffffffffu, mb, off));
-    const float m = Raw<T>::m_to_float(mb);
-    if (active && tl == 0) {
-      absmax[b] = m;
-      if (Raw<T>::nonfinite(mb)) raise_flag(flag, FLAG_NONFINITE);
-    }
-    const float inv32 = m > 0.0f ? __fdiv_rn((float)QMAX, m) : 0.0f;
-    const bool slow = !(inv32 <= 0x1p100f);  // reciprocal of a (sub)normal tiny absmax
-    const double inv64 = m > 0.0f ? __ddiv_rn((double)QMAX, (double)m) : 0.0;
-    uint8_t* out = codes + b * (int64_t)(B * BITS / 8);
-#pragma unroll
-    for (int c = 0; c < CH; ++c) {
-      float v[8];
-      uint32_t q[8];
-      Raw<T>::to_float(raw[c], v);
-      if (!slow) {
-        quant_chunk<QMAX>(v, inv32, inv64, q);
-      } else {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) q[i] = q_exact<QMAX>((double)v[i], inv64);
-      }
-      if (active) store_codes8<BITS>(out + (c * LANES + tl) * BITS, q);
-      if constexpr (DEQ) {
-        if (active) {
-          // code as an exact float: the low byte of q is the two's complement code
-          const float s32 = __fmul_rn(m, 1.0f / QMAX);
-          const bool ok16 = Out16<T>::in_range(m);
-          uint32_t h[4];
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const float c0 = (float)(int)(int8_t)(q[2 * i] & 0xFFu);
-            const float c1 = (float)(int)(int8_t)(q[2 * i + 1] & 0xFFu);
-            if (ok16) {
-              const float2 p = fmul2(make_float2(c0, c1), make_float2(s32, s32));
-              h[i] = Out16<T>::pack2(p.x, p.y);
-            } else {
-              const double s64 = scale_of<BITS>((double)m);
-              T a = from_f64<T>(__dmul_rn((double)c0, s64)), bb = from_f64<T>(__dmul_rn((double)c1, s64));
-              h[i] = (uint32_t)(*reinterpret_cast<uint16_t*>(&a)) | ((uint32_t)(*reinterpret_cast<uint16_t*>(&bb)) << 16);
-            }
-          }
-          const int e = (c * LANES + tl) * 8;
-          T* dst = deq_out + b * (int64_t)B + e;
-          if (e + 8 <= valid) {
-            *reinterpret_cast<uint4*>(dst) = make_uint4(h[0], h[1], h[2], h[3]);
-          } else {
-#pragma unroll
-            for (int i = 0; i < 8; ++i)
-              if (e + i < valid) reinterpret_cast<uint16_t*>(dst)[i] = (uint16_t)(h[i / 2] >> (16 * (i & 1)));
-          }
-        }
-      }
-    }
+    quant_team<T, BITS, LANES, EPL, Addr, DEQ>(x, addr, b, b < n_blocks, tl, codes, absmax, flag, deq_out);
   }
 }
 
@@ -1180,6 +1189,21 @@ template <int BITS> struct Vec16;
 template <> struct Vec16<8> { using T = uint4; };
 template <> struct Vec16<4> { using T = uint2; };
 
+// Source loads: read-only path (__ldg) when the sources cannot change during
+// the kernel, L2-coherent loads (ld.global.cg) when peers may still be
+// writing other parts of the same buffers.
+enum { kLdNC = 0, kLdCG = 1 };
+template <int MODE, typename V>
+__device__ __forceinline__ V ld_src(const V* p) {
+  if constexpr (MODE == kLdCG) return __ldcg(p);
+  else return __ldg(p);
+}
+template <int MODE, typename A>
+__device__ __forceinline__ double ld_absmax(const A* p, int64_t i) {
+  if constexpr (MODE == kLdCG) return (double)__ldcg(p + i);
+  else return absmax_f64<A>(p, i);
+}
+
 // acc[i] = RN64(acc[i] + RN64(code_i * s)) for the 16 codes in w -- the
 // reference's fold step (zs/quantizer.py:255-257, zs/collectives.py:71-75).
 // Each code becomes an exact double as 2^52+2^51+(code+bias) - (2^52+2^51+bias):
@@ -1217,63 +1241,157 @@ __device__ __forceinline__ void fold16(const typename Vec16<BITS>::T& w, double 
 
 // K3 fast path: lane = 16 contiguous elements, loads of up to 4 sources in
 // flight, f64 fold in source order from +0.0, one rounding to the output type.
+// One lane: 16 output elements of K3 starting at 16*u (see dequant_reduce16_kernel).
+template <int BITS, typename A, typename O, bool VALIDATE, int CG>
+__device__ __forceinline__ void dr_unit(const SrcTable& src, int n_src, int64_t u, int64_t B, bool pow2, int lg,
+                                        O* __restrict__ out, double post_scale, bool& bad) {
+  using V = typename Vec16<BITS>::T;
+  constexpr int SB = 4;
+  const int64_t e0 = u * 16;
+  const int64_t blk = pow2 ? (e0 >> lg) : e0 / B;
+  double acc[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) acc[i] = 0.0;
+  for (int s0 = 0; s0 < n_src; s0 += SB) {
+    V w[SB];
+    double sc[SB];
+#pragma unroll
+    for (int j = 0; j < SB; ++j) {
+      if (s0 + j < n_src) {
+        w[j] = ld_src<CG>(reinterpret_cast<const V*>(src.codes[s0 + j]) + u);
+        sc[j] = ld_absmax<CG, A>(reinterpret_cast<const A*>(src.absmax[s0 + j]), blk);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < SB; ++j) {
+      if (s0 + j >= n_src) break;
+      fold16<BITS, VALIDATE>(w[j], scale_of<BITS>(sc[j]), acc, bad);
+    }
+  }
+  if (post_scale != 1.0) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) acc[i] = __dmul_rn(acc[i], post_scale);
+  }
+  O* dst = out + e0;
+  if constexpr (sizeof(O) == 4) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      reinterpret_cast<float4*>(dst)[i] = make_float4(from_f64<float>(acc[4 * i]), from_f64<float>(acc[4 * i + 1]),
+                                                      from_f64<float>(acc[4 * i + 2]), from_f64<float>(acc[4 * i + 3]));
+  } else if constexpr (sizeof(O) == 8) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) reinterpret_cast<double2*>(dst)[i] = make_double2(acc[2 * i], acc[2 * i + 1]);
+  } else {
+    uint32_t h[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      O a = from_f64<O>(acc[2 * i]), b = from_f64<O>(acc[2 * i + 1]);
+      h[i] = (uint32_t)(*reinterpret_cast<uint16_t*>(&a)) | ((uint32_t)(*reinterpret_cast<uint16_t*>(&b)) << 16);
+    }
+    store_words<8>(dst, h);
+  }
+}
+
 template <int BITS, typename A, typename O, bool VALIDATE>
 __global__ void __launch_bounds__(256)
 dequant_reduce16_kernel(SrcTable src, int n_src, int64_t n, int64_t B, O* __restrict__ out, double post_scale,
                         uint32_t* __restrict__ flag) {
-  using V = typename Vec16<BITS>::T;
-  constexpr int SB = 4;
   const int64_t units = n / 16;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const bool pow2 = (B & (B - 1)) == 0;
   const int lg = pow2 ? __ffsll(B) - 1 : 0;
   bool bad = false;
-  for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < units; u += stride) {
-    const int64_t e0 = u * 16;
-    const int64_t blk = pow2 ? (e0 >> lg) : e0 / B;
-    double acc[16];
+  for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < units; u += stride)
+    dr_unit<BITS, A, O, VALIDATE, kLdNC>(src, n_src, u, B, pow2, lg, out, post_scale, bad);
+  if (bad) raise_flag(flag, FLAG_BADCODE);
+}
+
+// One team of LANES lanes: output block b of K2 (see drq16_kernel).
+template <int IBITS, typename IA, int OBITS, int LANES, bool VALIDATE, typename FO, int CG, int CGA = CG,
+          typename Src = SrcTable>
+__device__ __forceinline__ void drq_team(const Src& src, int n_src, int64_t n, int64_t B1, bool pow2, int lg,
+                                         int64_t b, int64_t n_blocks_out, int tl, uint8_t* __restrict__ codes,
+                                         double* __restrict__ absmax, uint32_t* __restrict__ flag,
+                                         FO* __restrict__ final_out, bool& bad) {
+  using V = typename Vec16<IBITS>::T;
+  constexpr int B2 = LANES * 16;
+  constexpr int QMAX = Codes<OBITS>::kQmax;
+  constexpr int SB = 4;
+  const int64_t e0 = b * B2 + (int64_t)tl * 16;
+  const bool active = b < n_blocks_out && e0 < n;  // n % 16 == 0: lanes are all-valid or all-empty
+  const int64_t u = e0 / 16;
+  const int64_t ib = pow2 ? (e0 >> lg) : e0 / B1;
+  double acc[16];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) acc[i] = 0.0;
-    for (int s0 = 0; s0 < n_src; s0 += SB) {
-      V w[SB];
-      double sc[SB];
+  for (int i = 0; i < 16; ++i) acc[i] = 0.0;
+  for (int s0 = 0; s0 < n_src; s0 += SB) {
+    V w[SB];
+    double sc[SB];
 #pragma unroll
-      for (int j = 0; j < SB; ++j) {
-        if (s0 + j < n_src) {
-          w[j] = __ldg(reinterpret_cast<const V*>(src.codes[s0 + j]) + u);
-          sc[j] = absmax_f64<A>(reinterpret_cast<const A*>(src.absmax[s0 + j]), blk);
-        }
+    for (int j = 0; j < SB; ++j) {
+      if (active && s0 + j < n_src) {
+        w[j] = ld_src<CG>(reinterpret_cast<const V*>(src.code_ptr(s0 + j)) + u);
+        sc[j] = ld_absmax<CGA, IA>(reinterpret_cast<const IA*>(src.abs_ptr(s0 + j)), ib);
       }
+    }
+    if (active) {
 #pragma unroll
       for (int j = 0; j < SB; ++j) {
         if (s0 + j >= n_src) break;
-        fold16<BITS, VALIDATE>(w[j], scale_of<BITS>(sc[j]), acc, bad);
+        fold16<IBITS, VALIDATE>(w[j], scale_of<IBITS>(sc[j]), acc, bad);
       }
-    }
-    if (post_scale != 1.0) {
-#pragma unroll
-      for (int i = 0; i < 16; ++i) acc[i] = __dmul_rn(acc[i], post_scale);
-    }
-    O* dst = out + e0;
-    if constexpr (sizeof(O) == 4) {
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-        reinterpret_cast<float4*>(dst)[i] = make_float4(from_f64<float>(acc[4 * i]), from_f64<float>(acc[4 * i + 1]),
-                                                        from_f64<float>(acc[4 * i + 2]), from_f64<float>(acc[4 * i + 3]));
-    } else if constexpr (sizeof(O) == 8) {
-#pragma unroll
-      for (int i = 0; i < 8; ++i) reinterpret_cast<double2*>(dst)[i] = make_double2(acc[2 * i], acc[2 * i + 1]);
-    } else {
-      uint32_t h[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        O a = from_f64<O>(acc[2 * i]), b = from_f64<O>(acc[2 * i + 1]);
-        h[i] = (uint32_t)(*reinterpret_cast<uint16_t*>(&a)) | ((uint32_t)(*reinterpret_cast<uint16_t*>(&b)) << 16);
-      }
-      store_words<8>(dst, h);
     }
   }
-  if (bad) raise_flag(flag, FLAG_BADCODE);
+  double mx = 0.0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) mx = fmax(mx, fabs(acc[i]));
+#pragma unroll
+  for (int off = LANES / 2; off >= 1; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+  if (b < n_blocks_out && tl == 0) {
+    absmax[b] = mx;
+    if (!(mx <= DBL_MAX)) raise_flag(flag, FLAG_NONFINITE);
+  }
+  if (active) {
+    const double inv = mx > 0.0 ? __ddiv_rn((double)QMAX, mx) : 0.0;
+    uint32_t q0[8], q1[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {  // |acc*inv| <= qmax: no clamp needed
+      q0[i] = (uint32_t)rint_f64(__dmul_rn(acc[i], inv));
+      q1[i] = (uint32_t)rint_f64(__dmul_rn(acc[8 + i], inv));
+    }
+    if constexpr (std::is_void<FO>::value) {
+      uint8_t* dst = codes + u * 2 * OBITS;
+      if constexpr (OBITS == 8) {
+        const uint2 a = pack8_int8(q0), c = pack8_int8(q1);
+        *reinterpret_cast<uint4*>(dst) = make_uint4(a.x, a.y, c.x, c.y);
+      } else {
+        *reinterpret_cast<uint2*>(dst) = make_uint2(pack8_int4(q0), pack8_int4(q1));
+      }
+    } else {
+      const double s2 = scale_of<OBITS>(mx);
+      double v[16];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        v[i] = __dadd_rn(0.0, __dmul_rn((double)(int)q0[i], s2));
+        v[8 + i] = __dadd_rn(0.0, __dmul_rn((double)(int)q1[i], s2));
+      }
+      FO* dst = final_out + e0;
+      if constexpr (sizeof(FO) == 4) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          reinterpret_cast<float4*>(dst)[i] = make_float4(from_f64<float>(v[4 * i]), from_f64<float>(v[4 * i + 1]),
+                                                          from_f64<float>(v[4 * i + 2]), from_f64<float>(v[4 * i + 3]));
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) reinterpret_cast<double2*>(dst)[i] = make_double2(v[2 * i], v[2 * i + 1]);
+      }
+    }
+  } else if (b < n_blocks_out && std::is_void<FO>::value) {
+    // zero padding of a partial last block (zs/quantizer.py:215-217)
+    uint8_t* dst = codes + u * 2 * OBITS;
+    if constexpr (OBITS == 8) *reinterpret_cast<uint4*>(dst) = make_uint4(0, 0, 0, 0);
+    else *reinterpret_cast<uint2*>(dst) = make_uint2(0, 0);
+  }
 }
 
 // K2 fast path: a team of LANES lanes owns one output block of B2 = 16*LANES
@@ -1288,11 +1406,7 @@ template <int IBITS, typename IA, int OBITS, int LANES, bool VALIDATE, typename 
 __global__ void __launch_bounds__(256)
 drq16_kernel(SrcTable src, int n_src, int64_t n, int64_t B1, int64_t n_blocks_out, uint8_t* __restrict__ codes,
              double* __restrict__ absmax, uint32_t* __restrict__ flag, FO* __restrict__ final_out = nullptr) {
-  using V = typename Vec16<IBITS>::T;
-  constexpr int B2 = LANES * 16;
   constexpr int TPW = 32 / LANES;
-  constexpr int QMAX = Codes<OBITS>::kQmax;
-  constexpr int SB = 4;
   const int lane = threadIdx.x & 31;
   const int tl = lane % LANES;
   const int team = lane / LANES;
@@ -1301,84 +1415,9 @@ drq16_kernel(SrcTable src, int n_src, int64_t n, int64_t B1, int64_t n_blocks_ou
   const bool pow2 = (B1 & (B1 - 1)) == 0;
   const int lg = pow2 ? __ffsll(B1) - 1 : 0;
   bool bad = false;
-  for (int64_t wb = gwarp * TPW; wb < n_blocks_out; wb += nwarp * TPW) {
-    const int64_t b = wb + team;
-    const int64_t e0 = b * B2 + (int64_t)tl * 16;
-    const bool active = b < n_blocks_out && e0 < n;  // n % 16 == 0: lanes are all-valid or all-empty
-    const int64_t u = e0 / 16;
-    const int64_t ib = pow2 ? (e0 >> lg) : e0 / B1;
-    double acc[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) acc[i] = 0.0;
-    for (int s0 = 0; s0 < n_src; s0 += SB) {
-      V w[SB];
-      double sc[SB];
-#pragma unroll
-      for (int j = 0; j < SB; ++j) {
-        if (active && s0 + j < n_src) {
-          w[j] = __ldg(reinterpret_cast<const V*>(src.codes[s0 + j]) + u);
-          sc[j] = absmax_f64<IA>(reinterpret_cast<const IA*>(src.absmax[s0 + j]), ib);
-        }
-      }
-      if (active) {
-#pragma unroll
-        for (int j = 0; j < SB; ++j) {
-          if (s0 + j >= n_src) break;
-          fold16<IBITS, VALIDATE>(w[j], scale_of<IBITS>(sc[j]), acc, bad);
-        }
-      }
-    }
-    double mx = 0.0;
-#pragma unroll
-    for (int i = 0; i < 16; ++i) mx = fmax(mx, fabs(acc[i]));
-#pragma unroll
-    for (int off = LANES / 2; off >= 1; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
-    if (b < n_blocks_out && tl == 0) {
-      absmax[b] = mx;
-      if (!(mx <= DBL_MAX)) raise_flag(flag, FLAG_NONFINITE);
-    }
-    if (active) {
-      const double inv = mx > 0.0 ? __ddiv_rn((double)QMAX, mx) : 0.0;
-      uint32_t q0[8], q1[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {  // |acc*inv| <= qmax: no clamp needed
-        q0[i] = (uint32_t)rint_f64(__dmul_rn(acc[i], inv));
-        q1[i] = (uint32_t)rint_f64(__dmul_rn(acc[8 + i], inv));
-      }
-      if constexpr (std::is_void<FO>::value) {
-        uint8_t* dst = codes + u * 2 * OBITS;
-        if constexpr (OBITS == 8) {
-          const uint2 a = pack8_int8(q0), c = pack8_int8(q1);
-          *reinterpret_cast<uint4*>(dst) = make_uint4(a.x, a.y, c.x, c.y);
-        } else {
-          *reinterpret_cast<uint2*>(dst) = make_uint2(pack8_int4(q0), pack8_int4(q1));
-        }
-      } else {
-        const double s2 = scale_of<OBITS>(mx);
-        double v[16];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          v[i] = __dadd_rn(0.0, __dmul_rn((double)(int)q0[i], s2));
-          v[8 + i] = __dadd_rn(0.0, __dmul_rn((double)(int)q1[i], s2));
-        }
-        FO* dst = final_out + e0;
-        if constexpr (sizeof(FO) == 4) {
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-            reinterpret_cast<float4*>(dst)[i] = make_float4(from_f64<float>(v[4 * i]), from_f64<float>(v[4 * i + 1]),
-                                                            from_f64<float>(v[4 * i + 2]), from_f64<float>(v[4 * i + 3]));
-        } else {
-#pragma unroll
-          for (int i = 0; i < 8; ++i) reinterpret_cast<double2*>(dst)[i] = make_double2(v[2 * i], v[2 * i + 1]);
-        }
-      }
-    } else if (b < n_blocks_out && std::is_void<FO>::value) {
-      // zero padding of a partial last block (zs/quantizer.py:215-217)
-      uint8_t* dst = codes + u * 2 * OBITS;
-      if constexpr (OBITS == 8) *reinterpret_cast<uint4*>(dst) = make_uint4(0, 0, 0, 0);
-      else *reinterpret_cast<uint2*>(dst) = make_uint2(0, 0);
-    }
-  }
+  for (int64_t wb = gwarp * TPW; wb < n_blocks_out; wb += nwarp * TPW)
+    drq_team<IBITS, IA, OBITS, LANES, VALIDATE, FO, kLdNC>(src, n_src, n, B1, pow2, lg, wb + team, n_blocks_out, tl,
+                                                           codes, absmax, flag, final_out, bad);
   if (bad) raise_flag(flag, FLAG_BADCODE);
 }
 

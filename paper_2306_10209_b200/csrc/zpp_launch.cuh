@@ -6,14 +6,24 @@
 
 namespace zpp {
 
+// SM budget for the next launches on this host thread (0 = the whole GPU).
+// Lets two stream-concurrent kernels (qgZ K1 of stage s+1 beside K2 of stage
+// s) split the SMs instead of the first launched one taking a full wave.
+inline thread_local int t_sm_cap = 0;
+
+struct SmBudget {
+  int saved;
+  explicit SmBudget(int sms) : saved(t_sm_cap) { t_sm_cap = sms; }
+  ~SmBudget() { t_sm_cap = saved; }
+};
+
 // one resident wave of CTAs (persistent-style grid-stride), capped by work
 template <typename K>
 inline int grid_for(K kernel, int threads, int64_t needed_ctas) {
-  static thread_local int dummy = 0;
-  (void)dummy;
   int occ = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, 0) != cudaSuccess || occ <= 0) occ = 1;
-  int64_t g = (int64_t)sm_count() * occ;
+  const int sms = (t_sm_cap > 0 && t_sm_cap < sm_count()) ? t_sm_cap : sm_count();
+  int64_t g = (int64_t)sms * occ;
   if (needed_ctas < g) g = needed_ctas;
   return (int)(g < 1 ? 1 : g);
 }

@@ -90,6 +90,18 @@ def main():
         o32 = comm.qgz_reduce_scatter(gt)
         comm.check()
         check(f"qgz f32 it{it}", np.array_equal(o32.cpu().numpy(), ref.astype(np.float32)))
+    # a second communicator and bucket size: 83 blocks per slice, stages 1
+    L2 = 2 * 16384 + 17 * 512
+    n2 = world * L2
+    grads2 = [bf16_bits(np.random.default_rng(400 + r).normal(size=n2) * 1e-3) for r in range(world)]
+    ref2 = O.qgz_2hop([gu.as_f64(g, "bf16") for g in grads2], X, Y, 1, 4, 512)[rank]
+    comm2 = Communicator(group_size=X, qgz_elems=n2, qgz_stages=1, qgz_cfg=zpp.QuantConfig(bit_width=4, block_size=512))
+    gt2 = gu.to_torch(grads2[rank], "bf16")
+    for it in range(3):
+        o2 = comm2.qgz_reduce_scatter(gt2, out_dtype=torch.float64)
+        comm2.check()
+        check(f"qgz bucket2 it{it}", np.array_equal(o2.cpu().numpy(), ref2))
+    comm2.close()
     # ---- process groups for the staged comparators ---------------------------
     mine_pg, cross_pg = make_groups(X)
     check("groups", dist.get_world_size(mine_pg) == X and dist.get_world_size(cross_pg) == Y)

@@ -20,11 +20,11 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _run(nproc, group, stages):
+def _run(nproc, group, stages, env=None):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
            os.path.join(HERE, "dist_worker.py"), "--group", str(group), "--stages", str(stages)]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env={**os.environ, **(env or {})})
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
 
 
@@ -37,6 +37,13 @@ def test_four_gpus_2x2():
     if torch.cuda.device_count() < 4:
         pytest.skip("needs 4 GPUs")
     _run(4, 2, 2)
+
+
+def test_four_gpus_1x4():
+    """One group of four (Y = 1: the hop-2 self-send fused into K2)."""
+    if torch.cuda.device_count() < 4:
+        pytest.skip("needs 4 GPUs")
+    _run(4, 4, 1)
 
 
 def test_eight_gpus_2x4():

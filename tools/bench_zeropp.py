@@ -46,14 +46,27 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())  # ms
 
-    res = {"world": world, "group_size": X}
+    sections = os.environ.get("ZPP_BENCH_SECTIONS", "qgz,hpz,step").split(",")
+    res = {"world": world, "group_size": X, "k1_sms": os.environ.get("ZPP_QGZ_K1_SMS")}
     group_pg, _ = make_groups(X)
 
     # ---- qgZ stage sweep --------------------------------------------------------
+    if "qgz" in sections:
+        qgz_sweep(res, X, world, dev, g, timed)
+    if "hpz" in sections:
+        hpz_layer(res, X, world, dev, g, timed, group_pg)
+    if "step" in sections:
+        step_13b(res, X, world, dev, g, timed)
+    if rank == 0:
+        print(json.dumps(res), flush=True)
+    dist.destroy_process_group()
+
+
+def qgz_sweep(res, X, world, dev, g, timed):
     bucket = 134_217_728
     grad = (torch.randn(bucket, generator=g, device=dev) * 1e-3).bfloat16()
     q = {}
-    for S in (1, 2, 4):
+    for S in [int(v) for v in os.environ.get("ZPP_BENCH_STAGES", "1,2,4,8").split(",")]:
         comm = Communicator(group_size=X, qgz_elems=bucket, qgz_stages=S,
                             qgz_cfg=zpp.QuantConfig(bit_width=4, block_size=512))
         out = torch.empty(bucket // world, dtype=torch.float32, device=dev)
@@ -64,6 +77,8 @@ def main():
     q["nccl_bf16_rs_ms"] = timed(lambda: nccl_reduce_scatter(grad, out=pb))
     res["qgz_256MiB"] = q
 
+
+def hpz_layer(res, X, world, dev, g, timed, group_pg):
     # ---- hpZ: GPT-1.3B layer ----------------------------------------------------
     h = 2048
     layer = 12 * h * h + 13 * h
@@ -85,6 +100,8 @@ def main():
     comm.close()
     res["hpz_gpt1.3b_layer"] = hp
 
+
+def step_13b(res, X, world, dev, g, timed):
     # ---- combined ZeRO++ step communication, one GPT-13B layer --------------------
     h = 5120
     layer = 12 * h * h + 13 * h
@@ -121,9 +138,6 @@ def main():
     res["gpt13b_layer_step_comm"] = {"layer_params": layer, "padded": layer_p, "zeropp_ms": t_zpp, "parts_ms": {"qwz": t_qwz, "hpz": t_hpz, "qgz": t_qgz},
                                      "zero3_nccl_ms": t_z3, "zero3_parts_ms": {"ag": t_ag, "rs": t_rs}, "speedup": t_z3 / t_zpp,
                                      "zeropp_40_layers_ms": 40 * t_zpp, "zero3_40_layers_ms": 40 * t_z3}
-    if rank == 0:
-        print(json.dumps(res), flush=True)
-    dist.destroy_process_group()
 
 
 if __name__ == "__main__":
