@@ -15,12 +15,12 @@ that every rank maps through CUDA IPC:
 * ``Communicator.qgz_reduce_scatter``  qgZ (zs/collectives.py:464-569): per
   stage K1 (reorder + quantize) -> group barrier -> K2 pulls the X intra-group
   messages over NVLink and requantizes -> cross barrier -> K3 pulls the Y
-  hop-2 segments and folds them in f64.
+  hop-2 segments and folds them in f64.  With one group, K2 writes the final
+  partition itself (hop 2 is a self-send).
 
 ``torch.distributed`` is plumbing only: it exchanges the 64-byte IPC handles
-once and provides the NCCL comparators (``nccl_*``, the fp16/bf16 ZeRO-3
-baseline collectives and a staged qwZ/qgZ that routes the same kernels through
-NCCL all-gather / all-to-all).
+once and provides the NCCL comparators (``nccl_allgather`` /
+``nccl_reduce_scatter``: the fp16/bf16 ZeRO-3 baseline collectives).
 """
 
 from __future__ import annotations
@@ -73,6 +73,14 @@ class SymLayout:
         hpz = _align(qwz + qwz_bytes)
         qgz = _align(hpz + hpz_bytes)
         return SymLayout(qwz=qwz, hpz=hpz, qgz=qgz, total=_align(qgz + qgz_bytes))
+
+
+def _check_buf(t: torch.Tensor, name: str, min_numel: int):
+    """The C ABI takes raw pointers: insist on dense CUDA tensors of sufficient size."""
+    if not t.is_cuda or not t.is_contiguous():
+        raise ValidationError(f"{name} must be a contiguous CUDA tensor")
+    if t.numel() < min_numel:
+        raise ValidationError(f"{name} has {t.numel()} elements, needs {min_numel}")
 
 
 def exchange_handles(handle: bytes, group=None) -> bytes:
@@ -153,8 +161,12 @@ class Communicator:
         if n > self.qwz_shard:
             raise ValidationError(f"shard has {n} elements, communicator was sized for {self.qwz_shard}")
         stride = out_stride or n
+        if stride < n:
+            raise ValidationError(f"out_stride {stride} is smaller than the shard ({n})")
+        _check_buf(shard, "shard", n)
         if out is None:
             out = torch.empty(stride * (self.world - 1) + n, dtype=out_dtype, device=shard.device)
+        _check_buf(out, "out", stride * (self.world - 1) + n)
         sec_ptr, sec_lo, sec_len = None, 0, 0
         if write_secondary:
             if self._secondary is None:
@@ -224,6 +236,9 @@ class Communicator:
             raise ValidationError("communicator has no hpZ secondary region")
         if out is None:
             out = torch.empty(self.hpz_sec * self.group_size, dtype=self.hpz_dtype, device=device())
+        _check_buf(out, "out", self.hpz_sec * self.group_size)
+        if out.element_size() != self._secondary.element_size():
+            raise ValidationError("hpZ output dtype must match the secondary shard's element size")
         _lib.check(self.lib.zpp_hpz_allgather(self.handle, self.layout.hpz, self.hpz_sec,
                                               self._secondary.element_size(), out.data_ptr(), self.flag.data_ptr(),
                                               stream_ptr()), "hpz_allgather")
@@ -236,8 +251,10 @@ class Communicator:
         n = int(grad.numel())
         if n != self.qgz_elems:
             raise ValidationError(f"gradient has {n} elements, communicator was sized for {self.qgz_elems}")
+        _check_buf(grad, "grad", n)
         if out is None:
             out = torch.empty(n // self.world, dtype=out_dtype, device=grad.device)
+        _check_buf(out, "out", n // self.world)
         _lib.check(self.lib.zpp_qgz_reduce_scatter(self.handle, self.layout.qgz, grad.data_ptr(),
                                                    dtype_code(grad.dtype), n, self.qgz_stages, int(reorder),
                                                    self.qgz_intra_cfg.bit_width, self.qgz_intra_cfg.block_size,
@@ -291,7 +308,7 @@ def _wrap_device(ptr: int, n: int, dtype: torch.dtype) -> torch.Tensor:
 
 
 # ---------------------------------------------------------------------------
-# NCCL comparators (the ZeRO-3 baseline collectives and a staged ZeRO++ route)
+# NCCL comparators (the ZeRO-3 baseline collectives)
 
 
 def nccl_allgather(shard: torch.Tensor, out: torch.Tensor | None = None, group=None) -> torch.Tensor:

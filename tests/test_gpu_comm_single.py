@@ -45,6 +45,16 @@ def test_world1_collectives():
         comm.check()
     with pytest.raises(zpp.ValidationError):
         comm.qwz_allgather(torch.zeros(n + 8, device="cuda", dtype=torch.float16))
+    # raw-pointer boundary: undersized / host / strided buffers are rejected before launch
+    xs = torch.from_numpy(x).cuda()
+    with pytest.raises(zpp.ValidationError):
+        comm.qwz_allgather(xs, out=torch.empty(n - 1, dtype=torch.float16, device="cuda"))
+    with pytest.raises(zpp.ValidationError):
+        comm.qwz_allgather(torch.from_numpy(x))
+    with pytest.raises(zpp.ValidationError):
+        comm.qgz_reduce_scatter(torch.zeros(8192, device="cuda")[::2])
+    with pytest.raises(zpp.ValidationError):
+        comm.hpz_allgather(out=torch.empty(n, dtype=torch.float32, device="cuda"))
     comm.close()
 
 
