@@ -311,3 +311,56 @@ def test_serialization_is_deterministic():
     x = torch.from_numpy(np.random.default_rng(5).normal(size=777)).cuda()
     cfg = zpp.QuantConfig(bit_width=4, block_size=64)
     assert zpp.quantize(x, cfg).to_bytes() == zpp.quantize(x, cfg).to_bytes()
+
+
+def _bf16_from_f64(v):
+    return gu.round_to(np.asarray(v, np.float64), "bf16")
+
+
+@pytest.mark.parametrize("bits", [4, 8])
+def test_exact_ties_bf16(bits):
+    """bf16 blocks whose elements sit EXACTLY on a half-integer after scaling
+    (x * 2*qmax / absmax odd): the reference's f64 rint goes to even.  These
+    are the common case for bf16/INT4 and all of them take the f64 fix-up."""
+    zpp = _zpp()
+    qmax = 2 ** (bits - 1) - 1
+    rng = np.random.default_rng(11 + bits)
+    blocks = []
+    while len(blocks) < 256:
+        m = float(_bf16_from_f64(np.exp(rng.normal() * 4)))
+        cand = _bf16_from_f64(rng.uniform(-m, m, size=8192))
+        t = cand.astype(np.float64) * (2 * qmax) / m
+        ties = cand[(np.abs(t - np.rint(t)) == 0) & (np.rint(t) % 2 == 1)]
+        if len(ties) < 16:
+            continue
+        blk = np.resize(ties, 511)
+        blocks.append(rng.permutation(np.concatenate([[m], blk])))
+    arr = np.concatenate(blocks)
+    x = torch.from_numpy(arr).to(torch.bfloat16).cuda()  # exact: every value is a bf16
+    q = zpp.quantize(x, zpp.QuantConfig(bit_width=bits, block_size=512))
+    c, s, _ = O.quantize(arr.astype(np.float64), bits, 512)
+    assert np.array_equal(q.codes.cpu().numpy(), c)
+    assert np.array_equal(q.scales.cpu().numpy(), s)
+
+
+@pytest.mark.parametrize("n_src", [1, 3, 5, 8])
+@pytest.mark.parametrize("bits,block,n", [(4, 512, 8192 + 512), (8, 2048, 3 * 2048 + 16), (8, 40, 999),
+                                          (4, 24, 1000)])
+def test_dequant_reduce_many_sources(n_src, bits, block, n):
+    """K3 (BlockCodec.reduce_final, zs/collectives.py:71-75): f64 fold in
+    source order from +0.0, for source counts around the 4-wide load batch,
+    fast (16-element) and general (odd block / length) paths; f64 output
+    bit-exact, fp32/fp16/bf16 outputs = the f64 result rounded once."""
+    zpp = _zpp()
+    rng = np.random.default_rng(n_src * 100 + bits)
+    cfg = zpp.QuantConfig(bit_width=bits, block_size=block)
+    vals = [rng.normal(size=n) * 10.0 ** rng.integers(-3, 3) for _ in range(n_src)]
+    qs = [zpp.quantize(torch.from_numpy(v).cuda(), cfg) for v in vals]
+    acc = np.zeros(n)
+    for v in vals:
+        c, s, _ = O.quantize(v, bits, block)
+        acc = acc + O.dequantize(c, s, n, bits, block)
+    assert np.array_equal(zpp.dequant_reduce(qs).cpu().numpy(), acc)
+    for dt in ("fp32", "fp16", "bf16"):
+        got = zpp.dequant_reduce(qs, getattr(torch, {"fp32": "float32", "fp16": "float16", "bf16": "bfloat16"}[dt]))
+        assert np.array_equal(got.double().cpu().numpy(), gu.round_to(acc, dt)), dt
