@@ -335,9 +335,59 @@ def build_volumes():
     print("volume cases:", len(rows))
 
 
+ENGINE_CASES = [
+    # (name, ZeroConfig kwargs, task kwargs, passthrough codecs)
+    ("plain", {}, {}, False),
+    ("qwz", dict(quantized_weight_gather=True), {}, False),
+    ("hpz", dict(hierarchical_secondary_gather=True), {}, False),
+    ("qgz", dict(quantized_grad_reduce=True), {}, False),
+    ("all_on", dict(quantized_weight_gather=True, hierarchical_secondary_gather=True, quantized_grad_reduce=True),
+     {}, False),
+    ("all_on_s2_2x4", dict(nodes=2, gpus_per_node=4, grad_stages=2, quantized_weight_gather=True,
+                           hierarchical_secondary_gather=True, quantized_grad_reduce=True), {}, False),
+    ("qgz_half_int8_intra", dict(quantized_grad_reduce=True, grad_quant_fraction=0.5,
+                                 grad_intra_quant=("q", 8, 256)), {}, False),
+    ("qgz_slice_scale_c09", dict(quantized_grad_reduce=True, grad_quant=("q", 4, 2560), seed=1),
+     dict(noise_sigma=0.1, input_scale_range=16.0), False),
+    ("routed_passthrough_c08", dict(quantized_weight_gather=True, hierarchical_secondary_gather=True,
+                                    quantized_grad_reduce=True), {}, True),
+]
+
+
+def _engine_cfg(kw):
+    kw = dict(kw)
+    for k, v in list(kw.items()):
+        if isinstance(v, tuple) and v and v[0] == "q":
+            kw[k] = zs.QuantConfig(bit_width=v[1], block_size=v[2])
+    return kw
+
+
+def build_engine(steps=40):
+    """Whole toy training runs of the reference TrainingEngine
+    (zs/engine.py:256-452): per-step losses and volumes, final master weights."""
+    import hashlib
+
+    rows = []
+    for name, zkw, tkw, passthrough in ENGINE_CASES:
+        eng = zs.TrainingEngine(zs.ToyTaskConfig(**tkw), zs.ZeroConfig(steps=steps, **_engine_cfg(zkw)))
+        if passthrough:
+            eng.weight_codec = zs.PassthroughCodec()
+            eng.grad_codec = zs.PassthroughCodec()
+        rec = eng.train()
+        rows.append(dict(name=name, zero=zkw, task=tkw, passthrough=passthrough, steps=steps,
+                         losses=[float(s.loss).hex() for s in rec.steps],
+                         volumes=[[repr(s.fwd_gather_volume), repr(s.bwd_gather_volume), repr(s.reduce_volume)]
+                                  for s in rec.steps],
+                         quantized_grads=[bool(s.quantized_grads) for s in rec.steps],
+                         initial_loss=float(rec.initial_loss).hex(), final_loss=float(rec.final_loss).hex(),
+                         diverged=rec.diverged, padded=rec.padded_params,
+                         master_sha256=hashlib.sha256(eng.master.tobytes()).hexdigest()))
+    with open(os.path.join(HERE, "engine.json"), "w") as f:
+        json.dump(rows, f, indent=1)
+    print("engine cases:", len(rows))
+
+
 if __name__ == "__main__":
-    build_quant()
-    build_fused()
-    build_collectives()
-    build_volumes()
-    build_wire()
+    which = sys.argv[1:] or ["quant", "fused", "collectives", "volumes", "wire", "engine"]
+    for name in which:
+        globals()["build_" + name]()

@@ -163,3 +163,30 @@ def test_secondary_gather_stays_on_node():
         assert led.physical_bytes(label=zpp.BWD_GATHER, cls=zpp.INTER) == 0
     off, _, _ = zpp.step_volumes(zpp.StepConfig(nodes=2, gpus_per_node=2), 1 << 16)
     assert off.physical_bytes(label=zpp.BWD_GATHER, cls=zpp.INTER) > 0
+
+
+def test_engine_mlp_gradient_matches_central_differences():
+    """The toy engine's analytic MLP gradient (zs/engine.py:196-220, checked
+    there by gradient_check :223-243) against central differences."""
+    from paper_2306_10209_b200 import engine as E
+
+    rng = np.random.default_rng(0)
+    dims = [4, 5, 3]
+    p = E.init_params(dims, rng)
+    x, y = rng.normal(size=(2, 4)), rng.normal(size=(2, 3))
+    _, g = E.mlp_loss_and_grad(p, x, y, dims)
+    num = np.zeros_like(g)
+    for i in range(len(p)):
+        d = np.zeros_like(p)
+        d[i] = 1e-6
+        num[i] = (E.mlp_loss_and_grad(p + d, x, y, dims)[0] - E.mlp_loss_and_grad(p - d, x, y, dims)[0]) / 2e-6
+    assert np.max(np.abs(g - num) / np.maximum(np.abs(num), 1e-8)) < 1e-4
+    assert E.param_count(E.ToyTaskConfig().layer_dims()) == 9928  # padded to 10240 over 4 ranks
+
+
+def test_engine_config_validation():
+    import paper_2306_10209_b200 as zpp
+
+    for kw in (dict(nodes=0), dict(steps=0), dict(lr=0.0), dict(grad_quant_fraction=1.5), dict(grad_stages=0)):
+        with pytest.raises(zpp.ValidationError):
+            zpp.ZeroConfig(**kw)
