@@ -35,9 +35,14 @@ from .topology import (
     INTRA,
     ClusterTopology,
     CollectiveTrace,
+    LatencyEstimate,
+    LinkParams,
     PhaseStats,
     TrafficLedger,
+    estimate_latency,
     normalized_cross_node_volume,
+    optimal_stages,
+    pipelined_seconds,
 )
 from .partitioner import PartitionSpec, build_partitions
 from .collectives import (
@@ -66,7 +71,8 @@ __all__ = [
     "FlatTensor", "QuantConfig", "QuantizedTensor", "QuantErrorStats", "quantize", "dequantize",
     "fused_dequant_reduce_quant", "dequant_reduce", "quant_error_stats",
     "INTRA", "INTER", "ClusterTopology", "TrafficLedger", "CollectiveTrace", "PhaseStats",
-    "normalized_cross_node_volume",
+    "normalized_cross_node_volume", "LinkParams", "LatencyEstimate", "estimate_latency", "pipelined_seconds",
+    "optimal_stages",
     "PartitionSpec", "build_partitions",
     "BlockCodec", "PassthroughCodec", "WirePayload", "as_codec", "GatherResult", "ReduceResult",
     "ReorderPermutation", "all_gather_baseline", "all_gather_qwz", "reduce_scatter_ring", "reorder_mapping",

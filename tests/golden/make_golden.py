@@ -379,6 +379,7 @@ def build_engine(steps=40):
                          volumes=[[repr(s.fwd_gather_volume), repr(s.bwd_gather_volume), repr(s.reduce_volume)]
                                   for s in rec.steps],
                          quantized_grads=[bool(s.quantized_grads) for s in rec.steps],
+                         csv_sha256=hashlib.sha256(rec.to_csv().encode()).hexdigest(),
                          initial_loss=float(rec.initial_loss).hex(), final_loss=float(rec.final_loss).hex(),
                          diverged=rec.diverged, padded=rec.padded_params,
                          master_sha256=hashlib.sha256(eng.master.tobytes()).hexdigest()))

@@ -44,6 +44,7 @@ def test_training_run_matches_reference_bit_for_bit(case):
     assert [[repr(s.fwd_gather_volume), repr(s.bwd_gather_volume), repr(s.reduce_volume)] for s in rec.steps] \
         == case["volumes"]
     assert [bool(s.quantized_grads) for s in rec.steps] == case["quantized_grads"]
+    assert hashlib.sha256(rec.to_csv().encode()).hexdigest() == case["csv_sha256"]  # incl. est_latency_s
     assert float(rec.final_loss).hex() == case["final_loss"] and rec.diverged == case["diverged"]
     assert hashlib.sha256(eng.master.tobytes()).hexdigest() == case["master_sha256"]
 

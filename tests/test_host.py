@@ -190,3 +190,30 @@ def test_engine_config_validation():
     for kw in (dict(nodes=0), dict(steps=0), dict(lr=0.0), dict(grad_quant_fraction=1.5), dict(grad_stages=0)):
         with pytest.raises(zpp.ValidationError):
             zpp.ZeroConfig(**kw)
+
+
+def test_c10_latency_pipeline_model():
+    """Acceptance c10 (pkg/tests/test_acceptance.py:344-380): one stage is the
+    plain two-phase sum, equal phases with free messages make two stages cost
+    75%, and optimal_stages matches a brute-force sweep with an interior optimum."""
+    import paper_2306_10209_b200 as zpp
+
+    trace = zpp.CollectiveTrace(label="step", phases=[zpp.PhaseStats(
+        "p", intra_messages=8, intra_bytes=300 * 10**9, inter_messages=8, inter_bytes=25 * 10**9)])
+    free = zpp.LinkParams(intra_alpha=0.0, intra_beta=300e9, inter_alpha=0.0, inter_beta=25e9)
+    t1 = zpp.estimate_latency(trace, free, stages=1).total_seconds
+    assert t1 == 2.0 and zpp.estimate_latency(trace, free, stages=2).total_seconds == 0.75 * t1
+    links = zpp.LinkParams(intra_alpha=1e-6, intra_beta=300e9, inter_alpha=1.25e-2, inter_beta=25e9)
+    im, ib, em, eb, _ = trace.totals()
+
+    def by_hand(s):
+        ti = links.intra_alpha * im * s + ib / links.intra_beta
+        te = links.inter_alpha * em * s + eb / links.inter_beta
+        return (ti + te) / s + (s - 1) * max(ti, te) / s
+
+    sweep = [by_hand(s) for s in range(1, 9)]
+    s_best, t_best = zpp.optimal_stages(trace, links, max_stages=8)
+    assert s_best == sweep.index(min(sweep)) + 1 and t_best == min(sweep) and 1 < s_best < 8
+    assert all(zpp.pipelined_seconds(trace, links, s) == sweep[s - 1] for s in range(1, 9))
+    with pytest.raises(zpp.ValidationError):
+        zpp.LinkParams(intra_beta=0.0)
