@@ -244,3 +244,37 @@ def test_memory_report_matches_reference():
         rows = json.load(f)
     for r in rows:
         assert zpp.memory_report(r["m"], r["world"], r["group"], r["k"]) == r["csv"], r
+
+
+def test_engine_parts_on_the_host():
+    """Engine pieces that need no GPU: layer views share the flat vector,
+    forward shapes and tanh range, per-rank gradient shards sum to the full
+    batch, the input-scale ramp, and the up-front codec check
+    (pkg/tests/test_engine.py restated)."""
+    import paper_2306_10209_b200 as zpp
+    from paper_2306_10209_b200 import engine as E
+
+    flat = np.zeros(E.param_count([3, 4, 2]))
+    (w0, _), (_, b1) = E._layers(flat, [3, 4, 2])
+    w0[1, 2], b1[0] = 7.0, -1.0
+    assert flat[6] == 7.0 and flat[3 * 4 + 4 + 4 * 2] == -1.0
+    rng = np.random.default_rng(0)
+    p = E.init_params([5, 8, 2], rng)
+    out, acts = E.mlp_forward(p, rng.normal(size=(7, 5)), [5, 8, 2])
+    assert out.shape == (7, 2) and len(acts) == 3 and np.all(np.abs(acts[1]) <= 1.0)
+    p = E.init_params([4, 6, 3], rng)
+    x, y = rng.normal(size=(8, 4)), rng.normal(size=(8, 3))
+    full = E.mlp_loss_and_grad(p, x, y, [4, 6, 3])[1]
+    parts = sum(E.mlp_loss_and_grad(p, x[i:i + 2], y[i:i + 2], [4, 6, 3], denom=8)[1] for i in range(0, 8, 2))
+    assert np.allclose(parts, full, rtol=0, atol=1e-12)
+    task = E.ToyTaskConfig(in_dim=8, hidden=(8,), out_dim=2, input_scale_range=16.0, eval_samples=16)
+    s = E.TrainingEngine(task, E.ZeroConfig(steps=1)).input_scales
+    assert s[-1] / s[0] == pytest.approx(16.0) and np.sum(s * s) == pytest.approx(8)
+    with pytest.raises(zpp.ValidationError):
+        E.TrainingEngine(E.ToyTaskConfig(input_scale_range=0.5), E.ZeroConfig(steps=1))
+    whole = zpp.QuantConfig(bit_width=4, mode="full_tensor")
+    with pytest.raises(zpp.ConfigError):
+        E.TrainingEngine(task, E.ZeroConfig(quantized_grad_reduce=True, grad_quant=whole))
+    E.TrainingEngine(task, E.ZeroConfig(grad_quant=whole))
+    eng = E.TrainingEngine(E.ToyTaskConfig(), E.ZeroConfig(steps=1))
+    assert (eng.m_params, eng.padded) == (9928, 10240)
