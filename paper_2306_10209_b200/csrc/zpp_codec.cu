@@ -198,54 +198,20 @@ static int run_gather(const SrcTable& t, int n_src, int rot, int64_t shard_len, 
     // fast 16-bit output path: one scale per 16-byte code load, aligned loads
     bool fast = block % (128 / BITS) == 0;
     for (int i = 0; i < n_src; ++i) fast = fast && aligned16(t.codes[i]);
-    if (fast && n_src > 1) {  // peers involved: latency-hiding cp.async pipeline
-      static const int pipe = [] {
-        const char* e = getenv("ZPP_GATHER_PIPE");
-        const int v = e ? atoi(e) : 8;
-        return (v == 4 || v == 6 || v == 8 || v == 12) ? v : 8;
-      }();
-      const int64_t tiles = ceil_div(ceil_div(shard_len, 128 / BITS), 256) * n_src;
-#define ZPP_PIPE(P)                                                                                    \
-  {                                                                                                    \
-    auto k = dequant16_pipe_kernel<BITS, O, P>;                                                        \
-    const int grid = grid_for(k, 256, tiles);                                                          \
-    k<<<grid, 256, 0, st>>>(t, n_src, rot, shard_len, block, reinterpret_cast<O*>(out),                \
-                            reinterpret_cast<O*>(sec_out), sec_lo, sec_len, vec_ok, flag, out_stride);            \
-    return check_cuda(cudaGetLastError(), "dequant16_pipe_kernel launch");                             \
-  }
-      // default: TMA bulk pipeline (ZPP_GATHER_MODE=pipe selects the per-thread cp.async ring)
-      static const int tma_cfg = [] {
-        const char* e = getenv("ZPP_GATHER_MODE");
-        if (e && std::string(e) == "pipe") return -1;
-        const char* c = getenv("ZPP_TMA_CFG");
-        return c ? atoi(c) : 0;
-      }();
-      if (tma_cfg >= 0) {
-        const int64_t units = ceil_div(shard_len, 128 / BITS);
-#define ZPP_TMA(S, TU)                                                                                 \
-  {                                                                                                    \
-    auto k = dequant16_tma_kernel<BITS, O, S, TU>;                                                     \
-    const int smem = S * TU * 16 + S * 8;                                                              \
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);                        \
-    int occ = 0;                                                                                       \
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 256, smem);                                 \
-    const int grid = (int)std::min<int64_t>((int64_t)sm_count() * std::max(occ, 1),                  \
-                                            ceil_div(units, TU) * n_src);                              \
-    k<<<grid, 256, smem, st>>>(t, n_src, rot, shard_len, block, reinterpret_cast<O*>(out),             \
-                            reinterpret_cast<O*>(sec_out), sec_lo, sec_len, vec_ok, flag, out_stride);            \
-    return check_cuda(cudaGetLastError(), "dequant16_tma_kernel launch");                              \
-  }
-        if (tma_cfg == 1) ZPP_TMA(8, 512)
-        if (tma_cfg == 2) ZPP_TMA(4, 1024)
-        if (tma_cfg == 3) ZPP_TMA(3, 2048)
-        ZPP_TMA(4, 512)
-#undef ZPP_TMA
-      }
-      if (pipe == 4) ZPP_PIPE(4)
-      if (pipe == 6) ZPP_PIPE(6)
-      if (pipe == 12) ZPP_PIPE(12)
-      ZPP_PIPE(8)
-#undef ZPP_PIPE
+    if (fast && n_src > 1) {
+      // peers involved: TMA bulk copies of each source's codes into a 4-stage
+      // shared ring hide the NVLink latency (4 x 512 units of 16 code bytes)
+      constexpr int S = 4, TU = 512;
+      auto k = dequant16_tma_kernel<BITS, O, S, TU>;
+      const int smem = S * TU * 16 + S * 8;
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      int occ = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 256, smem);
+      const int64_t units = ceil_div(shard_len, 128 / BITS);
+      const int grid = (int)std::min<int64_t>((int64_t)sm_count() * std::max(occ, 1), ceil_div(units, TU) * n_src);
+      k<<<grid, 256, smem, st>>>(t, n_src, rot, shard_len, block, reinterpret_cast<O*>(out),
+                                 reinterpret_cast<O*>(sec_out), sec_lo, sec_len, vec_ok, flag, out_stride);
+      return check_cuda(cudaGetLastError(), "dequant16_tma_kernel launch");
     }
     if (fast) {
       auto k = dequant16_kernel<BITS, O>;

@@ -704,87 +704,6 @@ dequant16_kernel(SrcTable src, int n_src, int rot, int64_t shard_len, int64_t B,
 }
 
 // ---------------------------------------------------------------------------
-// K4 over NVLink: the same decode fed by a per-thread cp.async pipeline.  A
-// CTA tile is 256 units of 16 code bytes (one per thread); each thread keeps
-// PIPE-1 of its own 16-byte copies in flight in shared memory (LDGSTS works on
-// peer-mapped addresses), so the remote-read latency (~2 us over NVLink) is
-// hidden without holding registers and without any CTA-wide barrier: a thread
-// only ever reads back the bytes it copied itself.
-
-template <int BITS, typename O, int PIPE>
-__global__ void __launch_bounds__(256, 4)
-dequant16_pipe_kernel(SrcTable src, int n_src, int rot, int64_t shard_len, int64_t B, O* __restrict__ out,
-                      O* __restrict__ sec_out, int64_t sec_lo, int64_t sec_len, int vec_ok,
-                      uint32_t* __restrict__ flag, int64_t out_stride) {
-  constexpr int E = Unit16B<BITS>::E;
-  __shared__ uint4 ring[PIPE][256];
-  const int tid = threadIdx.x;
-  const int units = (int)((shard_len + E - 1) / E);
-  const int tiles = (units + 255) / 256;
-  const int n_tiles = tiles * n_src;
-  const bool pow2 = (B & (B - 1)) == 0;
-  const int lg = pow2 ? __ffsll(B) - 1 : 0;
-  bool bad = false;
-  // tile k of this CTA: g = blockIdx.x + k * gridDim.x
-  auto src_of = [&](int g, int& s, int& unit) {
-    const int t = g / n_src;
-    s = g - t * n_src + rot;
-    if (s >= n_src) s -= n_src;
-    unit = t * 256 + tid;
-  };
-  auto issue = [&](int g, int slot) {
-    if (g < n_tiles) {
-      int s, unit;
-      src_of(g, s, unit);
-      if (unit < units) {
-        const uint4* gp = reinterpret_cast<const uint4*>(src.codes[s]) + unit;
-        const uint32_t sp = (uint32_t)__cvta_generic_to_shared(&ring[slot][tid]);
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sp), "l"(gp) : "memory");
-      }
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  };
-  int g = blockIdx.x;
-#pragma unroll
-  for (int k = 0; k < PIPE - 1; ++k) issue(g + k * (int)gridDim.x, k);
-  for (int k = 0; g < n_tiles; ++k, g += gridDim.x) {
-    asm volatile("cp.async.wait_group %0;" ::"n"(PIPE - 2) : "memory");
-    const int slot = k % PIPE;
-    const uint4 w = ring[slot][tid];
-    issue(g + (PIPE - 1) * (int)gridDim.x, (k + PIPE - 1) % PIPE);
-    int s, unit;
-    src_of(g, s, unit);
-    if (unit >= units) continue;
-    bad |= bad_codes(w, BITS);
-    const int64_t e0 = (int64_t)unit * E;
-    const float m = __ldg(reinterpret_cast<const float*>(src.absmax[s]) + (pow2 ? (e0 >> lg) : e0 / B));
-    uint32_t h[E / 2];
-    decode16_any<BITS, O>(w, m, h);
-    const int cnt = (int)min((int64_t)E, shard_len - e0);
-    const int64_t oi = (int64_t)s * out_stride + e0;
-    if (vec_ok && cnt == E) {
-      store_words<E / 2>(out + oi, h);
-    } else {
-#pragma unroll
-      for (int i = 0; i < E; ++i)
-        if (i < cnt) store_scalar<O>(out + oi, i, h[i / 2] >> (16 * (i & 1)));
-    }
-    if (sec_out != nullptr && oi + cnt > sec_lo && oi < sec_lo + sec_len) {
-      const int64_t k0 = oi - sec_lo;
-      if (vec_ok && cnt == E && k0 >= 0 && k0 + E <= sec_len) {
-        store_words<E / 2>(sec_out + k0, h);
-      } else {
-#pragma unroll
-        for (int i = 0; i < E; ++i)
-          if (i < cnt && k0 + i >= 0 && k0 + i < sec_len) store_scalar<O>(sec_out + k0, i, h[i / 2] >> (16 * (i & 1)));
-      }
-    }
-  }
-  asm volatile("cp.async.wait_all;" ::: "memory");
-  if (bad) raise_flag(flag, FLAG_BADCODE);
-}
-
-// ---------------------------------------------------------------------------
 // K4 over NVLink, TMA variant: one elected thread streams TILE-byte tiles of
 // codes from the (peer) source with cp.async.bulk into a STAGES-deep shared
 // ring, completion tracked by mbarrier transaction counts; all 256 threads

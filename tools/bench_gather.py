@@ -21,6 +21,6 @@ def timed(fn, steps=20):
 t = timed(lambda: comm.qwz_allgather(x, out=out)); comm.check()
 ingress = (world - 1) * (n + n // 2048 * 4)
 if rank == 0:
-    print(json.dumps({"pipe": os.environ.get("ZPP_GATHER_PIPE", "8"), "world": world, "ms": t,
+    print(json.dumps({"world": world, "ms": t,
                       "GBps_value": world * 2 * M / t / 1e6, "ingress_GBps_step": ingress / t / 1e6}), flush=True)
 comm.close(); dist.destroy_process_group()
