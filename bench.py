@@ -31,7 +31,22 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
-os.environ.setdefault("NCCL_DEBUG", "WARN")  # keep stdout to the one JSON line
+# stdout carries exactly one JSON line: everything else that writes to fd 1
+# (NCCL's version banner, library warnings) is sent to stderr, and the line is
+# written to a duplicate of the original stdout.
+_JSON_FD = None
+
+
+def _claim_stdout():
+    global _JSON_FD
+    if _JSON_FD is None:
+        sys.stdout.flush()
+        _JSON_FD = os.dup(1)
+        os.dup2(2, 1)
+
+
+def emit(line: dict) -> None:
+    os.write(_JSON_FD, (json.dumps(line) + "\n").encode())
 
 METRIC = "qwZ/qgZ effective GB/s at 1/2/4/8 B200; quant kernel HBM GB/s vs 8 TB/s"
 M_PARAMS = 1_300_004_864           # 1.3e9 rounded up to a multiple of 8 * 2048
@@ -171,7 +186,7 @@ def run_reference(args):
                                    "zs/quantizer.py quantize+dequantize, block-parallel over host threads"},
         "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
     return 0
 
 
@@ -186,9 +201,19 @@ def run_ours(args):
     rank, world, local = dist_env()
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    # ZPP_OVERSUBSCRIBE=1 (functional check only, never a bench number): more
+    # ranks than GPUs, e.g. the 8-rank 2x4 layout on a 4-GPU box.  NCCL refuses
+    # duplicate devices, so the host plumbing runs on gloo and the NCCL
+    # comparators are skipped.
+    oversub = os.environ.get("ZPP_OVERSUBSCRIBE") == "1"
+    if oversub:
+        local %= torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if oversub:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     lib = _lib.load()
     dev = torch.device("cuda", local)
     shard_len = M_PARAMS // world
@@ -209,7 +234,7 @@ def run_ours(args):
     def max_over_ranks(x: float) -> float:
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if oversub else dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -333,7 +358,7 @@ def run_ours(args):
 
     # ---- comparators and qgZ ---------------------------------------------------
     extra = {}
-    if world > 1:
+    if world > 1 and not oversub:
         t_nccl = timed(lambda: nccl_allgather(shard, out=out), args.steps, 2)
         extra["nccl_fp16_allgather"] = {"value": world * 2 * M_PARAMS / t_nccl / 1e9, "unit": "GB/s",
                                         "ms_per_step": t_nccl * 1e3}
@@ -349,12 +374,23 @@ def run_ours(args):
                     "effective_GBps": world * 2 * QGZ_BUCKET * (world - 1) / world / t_qgz / 1e9 if world > 1 else
                     2 * QGZ_BUCKET / t_qgz / 1e9,
                     "wire_bytes_per_gpu": wire}
-    if world > 1:
+    if world > 1 and not oversub:
         gb = grad.clone()
         pb = torch.empty(QGZ_BUCKET // world, dtype=torch.bfloat16, device=dev)
         t_rs = timed(lambda: nccl_reduce_scatter(gb, out=pb), args.steps, 2)
         extra["nccl_bf16_reduce_scatter"] = {"ms_per_bucket": t_rs * 1e3,
                                              "effective_GBps": world * 2 * QGZ_BUCKET * (world - 1) / world / t_rs / 1e9}
+
+    extra["hpz"] = hpz_leg(comm_cls=Communicator, world=world, dev=dev, g=g, timed=lambda f: timed(f, args.steps, 2),
+                           oversub=oversub, nccl_allgather=nccl_allgather)
+    extra["zeropp_step_13b_layer"] = step_leg(world=world, dev=dev, g=g, timed=lambda f: timed(f, max(5, args.steps // 2), 2),
+                                              oversub=oversub, comm_cls=Communicator, zpp=zpp,
+                                              nccl_allgather=nccl_allgather, nccl_reduce_scatter=nccl_reduce_scatter)
+    extra["params_per_s"] = {"qwz": world * M_PARAMS / t_step, "qgz": world * QGZ_BUCKET / t_qgz,
+                             "note": "whole-job parameters (or gradients) delivered per second"}
+    if world > 1:
+        extra["nvlink_nominal"] = {"peak": 900.0, "unit": "GB/s", "qwz_ingress_frac": (world - 1) * qbytes / kg / 1e9 / 900.0,
+                                   "qgz_wire_frac": wire / t_qgz / 1e9 / 900.0}
 
     line = None
     if rank == 0:
@@ -368,7 +404,8 @@ def run_ours(args):
                                    + (" (W=1: quantize->dequantize round trip)" if world == 1 else " (NVLink P2P)"),
                        "M": M_PARAMS, "shard_elems": shard_len, "quant": "int8/2048", "out_dtype": "fp16",
                        "parallelism": f"zero3-dp{world}", "groups": f"{world // comm.group_size}x{comm.group_size}",
-                       "l2": "inputs and outputs larger than L2 (shard + 2.6 GB fp16 output per step), no flush"},
+                       "l2": "inputs and outputs larger than L2 (shard + 2.6 GB fp16 output per step), no flush"}
+                      | ({"oversubscribed": "functional check, ranks share GPUs: not a measurement"} if oversub else {}),
             "roofline": roof,
             "cpu_baseline": {"value": cpu_gbs, "unit": "GB/s", "cores": threads, "kind": "port",
                              "sample": f"{1 << 25} fp16 elements, numpy oracle port of zs/quantizer.py "
@@ -379,11 +416,92 @@ def run_ours(args):
                     "fp16_allgather_ingress_bytes_per_gpu": (world - 1) * 2 * shard_len},
         }
         line.update(extra)
-        print(json.dumps(line), flush=True)
+        emit(line)
     comm.close()
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def _pad(n: int, align: int) -> int:
+    return (n + align - 1) // align * align
+
+
+def hpz_leg(*, comm_cls, world, dev, g, timed, oversub, nccl_allgather):
+    """BASELINE configs[2]: hpZ gather of one GPT-1.3B layer (12h^2+13h, h=2048)
+    inside a group of min(N, 4) consecutive GPUs, vs NCCL's full-box and group
+    fp16 all-gathers.  The secondary shard is written through by the qwZ gather
+    (zs/engine.py:364-370)."""
+    import torch
+
+    from paper_2306_10209_b200.dist import make_groups
+
+    X = min(world, 4)
+    h = 2048
+    layer = 12 * h * h + 13 * h
+    layer_p = _pad(layer, world * 2048)
+    sec = layer_p // X
+    comm = comm_cls(group_size=X, qwz_shard=layer_p // world, hpz_sec=sec)
+    w = (torch.randn(layer_p // world, generator=g, device=dev) * 0.02).half()
+    comm.qwz_allgather(w, write_secondary=True)
+    comm.check()
+    out = torch.empty(layer_p, dtype=torch.float16, device=dev)
+    t = timed(lambda: comm.hpz_allgather(out=out))
+    comm.check()
+    comm.close()
+    ingress = (X - 1) * sec * 2
+    res = {"workload": "hpZ fp16 gather of one GPT-1.3B layer inside a group", "layer_params": layer,
+           "padded": layer_p, "group_size": X, "ms": t * 1e3, "ingress_bytes_per_gpu": ingress,
+           "ingress_GBps": ingress / t / 1e9, "cross_group_bytes": 0}
+    if world > 1 and not oversub:
+        full_out = torch.empty(layer_p, dtype=torch.float16, device=dev)
+        res["nccl_fullbox_fp16_ag_ms"] = timed(lambda: nccl_allgather(w, out=full_out)) * 1e3
+        if X < world:
+            group_pg, _ = make_groups(X)
+            gs = torch.empty(sec, dtype=torch.float16, device=dev)
+            res["nccl_group_fp16_ag_ms"] = timed(lambda: nccl_allgather(gs, out=out, group=group_pg)) * 1e3
+    return res
+
+
+def step_leg(*, world, dev, g, timed, oversub, comm_cls, zpp, nccl_allgather, nccl_reduce_scatter):
+    """BASELINE configs[4]: the communication of one GPT-13B layer (h=5120) of a
+    ZeRO++ step -- forward qwZ (INT8/2048, writes the hpZ secondary), backward
+    hpZ gather inside the group, gradient qgZ (INT4/512, S=2) -- vs ZeRO-3's
+    fp16 all-gather x2 + bf16 reduce-scatter (NCCL)."""
+    import torch
+
+    X = min(world, 4)
+    h = 5120
+    layer = 12 * h * h + 13 * h
+    layer_p = _pad(layer, world * 2048 * 4)
+    comm = comm_cls(group_size=X, qwz_shard=layer_p // world, hpz_sec=layer_p // X, qgz_elems=layer_p,
+                    qgz_stages=2, qgz_cfg=zpp.QuantConfig(bit_width=4, block_size=512))
+    w = (torch.randn(layer_p // world, generator=g, device=dev) * 0.02).half()
+    gl = (torch.randn(layer_p, generator=g, device=dev) * 1e-3).bfloat16()
+    wout = torch.empty(layer_p, dtype=torch.float16, device=dev)
+    gout = torch.empty(layer_p // world, dtype=torch.float32, device=dev)
+
+    def zeropp_layer():
+        comm.qwz_allgather(w, out=wout, write_secondary=True)
+        comm.hpz_allgather(out=wout)
+        comm.qgz_reduce_scatter(gl, out=gout)
+
+    t = timed(zeropp_layer)
+    comm.check()
+    comm.close()
+    res = {"workload": "fwd qwZ + bwd hpZ + grad qgZ of one GPT-13B layer", "layer_params": layer,
+           "padded": layer_p, "groups": f"{world // X}x{X}", "zeropp_ms": t * 1e3, "zeropp_40_layers_ms": 40e3 * t}
+    if world > 1 and not oversub:
+        bout = torch.empty(layer_p // world, dtype=torch.bfloat16, device=dev)
+
+        def zero3_layer():
+            nccl_allgather(w, out=wout)
+            nccl_allgather(w, out=wout)
+            nccl_reduce_scatter(gl, out=bout)
+
+        t3 = timed(zero3_layer)
+        res.update({"zero3_nccl_ms": t3 * 1e3, "speedup_vs_zero3": t3 / t})
+    return res
 
 
 def main():
@@ -393,6 +511,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     args = ap.parse_args()
+    _claim_stdout()
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":

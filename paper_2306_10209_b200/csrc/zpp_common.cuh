@@ -57,6 +57,11 @@ __device__ __forceinline__ int rint_f64(double t) {
   return __double2loint(__dadd_rn(t, kMagic52));
 }
 
+// max(mx, a) for a running absmax mx >= 0 as one DSETP and two selects (fmax
+// also handles signaling NaNs: 8 instructions in SASS).  Like fmax it keeps mx
+// when a is NaN and keeps +inf, so the callers' !(mx <= DBL_MAX) flag is unchanged.
+__device__ __forceinline__ double dmax_nn(double mx, double a) { return a > mx ? a : mx; }
+
 constexpr float kMagic23 = 12582912.0f;  // 1.5 * 2^23: x + kMagic23 rounds x to an integer
 // quantize fast-path guard: |e| <= 0.5 - 2^-15 (see quant_chunk in zpp_kernels.cuh)
 constexpr float kTieGuard = 0.5f - 3.0517578125e-05f;

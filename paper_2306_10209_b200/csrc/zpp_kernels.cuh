@@ -1071,10 +1071,10 @@ drq_reg_kernel(SrcTable src, int n_src, int64_t n, int64_t B1, int64_t n_blocks_
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         if ((c0 + h) * 8 + i >= n) acc[h][i] = 0.0;  // zero padding like the reference
-        mx = fmax(mx, fabs(acc[h][i]));
+        mx = dmax_nn(mx, fabs(acc[h][i]));
       }
 #pragma unroll
-    for (int off = LANES / 2; off >= 1; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+    for (int off = LANES / 2; off >= 1; off >>= 1) mx = dmax_nn(mx, __shfl_xor_sync(0xffffffffu, mx, off));
     if (active && tl == 0) {
       absmax[b] = mx;
       if (!(mx <= DBL_MAX)) raise_flag(flag, FLAG_NONFINITE);
@@ -1263,9 +1263,9 @@ __device__ __forceinline__ void drq_team(const Src& src, int n_src, int64_t n, i
   }
   double mx = 0.0;
 #pragma unroll
-  for (int i = 0; i < 16; ++i) mx = fmax(mx, fabs(acc[i]));
+  for (int i = 0; i < 16; ++i) mx = dmax_nn(mx, fabs(acc[i]));
 #pragma unroll
-  for (int off = LANES / 2; off >= 1; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+  for (int off = LANES / 2; off >= 1; off >>= 1) mx = dmax_nn(mx, __shfl_xor_sync(0xffffffffu, mx, off));
   if (b < n_blocks_out && tl == 0) {
     absmax[b] = mx;
     if (!(mx <= DBL_MAX)) raise_flag(flag, FLAG_NONFINITE);

@@ -50,3 +50,13 @@ def test_eight_gpus_2x4():
     if torch.cuda.device_count() < 8:
         pytest.skip("needs 8 GPUs")
     _run(8, 4, 1)
+
+
+def test_eight_ranks_2x4_oversubscribed():
+    """The driver's 8-GPU layout (2 groups x 4, K3 + cross barrier with X = 4)
+    on a smaller box: two ranks per GPU, still one process per rank and peer
+    memory through CUDA IPC (see ZPP_OVERSUBSCRIBE in dist_worker.py)."""
+    n = torch.cuda.device_count()
+    if n < 2 or n >= 8:
+        pytest.skip("needs 2..7 GPUs (8 run test_eight_gpus_2x4)")
+    _run(8, 4, 1, env={"ZPP_OVERSUBSCRIBE": "1"})
