@@ -1127,7 +1127,10 @@ __device__ __forceinline__ double ld_absmax(const A* p, int64_t i) {
 // reference's fold step (zs/quantizer.py:255-257, zs/collectives.py:71-75).
 // Each code becomes an exact double as 2^52+2^51+(code+bias) - (2^52+2^51+bias):
 // one PRMT builds the low word, one DADD removes the bias.
-template <int BITS, bool VALIDATE>
+// ASSIGN (first source of a fold): acc[i] = RN64(code_i * s), which equals
+// RN64(+0.0 + RN64(code_i * s)) because the product is never -0.0 (s > 0 and
+// codes are integers), so the reference's fold from +0.0 is reproduced exactly.
+template <int BITS, bool VALIDATE, bool ASSIGN = false>
 __device__ __forceinline__ void fold16(const typename Vec16<BITS>::T& w, double s, double (&acc)[16], bool& bad) {
   const uint32_t* ww = reinterpret_cast<const uint32_t*>(&w);
   if constexpr (BITS == 8) {
@@ -1138,7 +1141,8 @@ __device__ __forceinline__ void fold16(const typename Vec16<BITS>::T& w, double 
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const double c = __dsub_rn(__hiloint2double(0x43380000, (int)__byte_perm(b, 0, 0x4440 + j)), Bias<8>::kD);
-        acc[4 * k + j] = __dadd_rn(acc[4 * k + j], __dmul_rn(c, s));
+        if constexpr (ASSIGN) acc[4 * k + j] = __dmul_rn(c, s);
+        else acc[4 * k + j] = __dadd_rn(acc[4 * k + j], __dmul_rn(c, s));
       }
     }
   } else {
@@ -1151,8 +1155,13 @@ __device__ __forceinline__ void fold16(const typename Vec16<BITS>::T& w, double 
       for (int j = 0; j < 4; ++j) {
         const double c0 = __dsub_rn(__hiloint2double(0x43380000, (int)__byte_perm(ev, 0, 0x4440 + j)), Bias<4>::kD);
         const double c1 = __dsub_rn(__hiloint2double(0x43380000, (int)__byte_perm(od, 0, 0x4440 + j)), Bias<4>::kD);
-        acc[8 * k + 2 * j] = __dadd_rn(acc[8 * k + 2 * j], __dmul_rn(c0, s));
-        acc[8 * k + 2 * j + 1] = __dadd_rn(acc[8 * k + 2 * j + 1], __dmul_rn(c1, s));
+        if constexpr (ASSIGN) {
+          acc[8 * k + 2 * j] = __dmul_rn(c0, s);
+          acc[8 * k + 2 * j + 1] = __dmul_rn(c1, s);
+        } else {
+          acc[8 * k + 2 * j] = __dadd_rn(acc[8 * k + 2 * j], __dmul_rn(c0, s));
+          acc[8 * k + 2 * j + 1] = __dadd_rn(acc[8 * k + 2 * j + 1], __dmul_rn(c1, s));
+        }
       }
     }
   }
@@ -1337,6 +1346,107 @@ drq16_kernel(SrcTable src, int n_src, int64_t n, int64_t B1, int64_t n_blocks_ou
   for (int64_t wb = gwarp * TPW; wb < n_blocks_out; wb += nwarp * TPW)
     drq_team<IBITS, IA, OBITS, LANES, VALIDATE, FO, kLdNC>(src, n_src, n, B1, pow2, lg, wb + team, n_blocks_out, tl,
                                                            codes, absmax, flag, final_out, bad);
+  if (bad) raise_flag(flag, FLAG_BADCODE);
+}
+
+// ---------------------------------------------------------------------------
+// K2 fixed fan-in fast path (the qgZ hop-1 reduce, zs/collectives.py:519-527):
+// NSRC sources known at compile time, fp32 absmax from K1, 512-element output
+// blocks (one warp per block, lane = 16 contiguous elements).  Codes are
+// always validated (-8 / -128 raise IntegrityError, zs/quantizer.py:233-235):
+// a few integer ops per 16 codes.
+// Against drq16_kernel it drops the runtime source loop and its predicates,
+// the +0.0 initialisation (first source assigns, see fold16), and the
+// small-absmax branch of the scale division (fp32 absmax is never below
+// 2^-149, inside div_q's exactness premise).  Same arithmetic, same bits.
+template <int Q>
+__device__ __forceinline__ double div_q_f32(float m) {
+  constexpr double r = 1.0 / Q;
+  const double md = (double)m;
+  const double q0 = __dmul_rn(md, r);
+  const double e = __fma_rn(-q0, (double)Q, md);
+  return __fma_rn(e, r, q0);
+}
+
+template <int IBITS, int OBITS, int NSRC, typename FO = void>
+__global__ void __launch_bounds__(256)
+drq_fast_kernel(SrcTable src, int64_t n, int lg1, int64_t n_blocks_out, uint8_t* __restrict__ codes,
+                double* __restrict__ absmax, uint32_t* __restrict__ flag, FO* __restrict__ final_out = nullptr) {
+  using V = typename Vec16<IBITS>::T;
+  constexpr int QMAX = Codes<OBITS>::kQmax;
+  const int tl = threadIdx.x & 31;
+  const int64_t nwarp = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  bool bad = false;
+  for (int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < n_blocks_out; b += nwarp) {
+    const int64_t e0 = b * 512 + (int64_t)tl * 16;
+    const bool active = e0 < n;  // n % 16 == 0: lanes are all-valid or all-empty
+    const int64_t u = e0 >> 4;
+    const int64_t ib = e0 >> lg1;
+    V w[NSRC];
+    float m[NSRC];
+#pragma unroll
+    for (int j = 0; j < NSRC; ++j) {
+      if (active) {
+        w[j] = __ldg(reinterpret_cast<const V*>(src.codes[j]) + u);
+        m[j] = __ldg(reinterpret_cast<const float*>(src.absmax[j]) + ib);
+      } else {
+        w[j] = V{};
+        m[j] = 0.0f;
+      }
+    }
+    double acc[16];
+    fold16<IBITS, true, true>(w[0], div_q_f32<Codes<IBITS>::kQmax>(m[0]), acc, bad);
+#pragma unroll
+    for (int j = 1; j < NSRC; ++j) fold16<IBITS, true>(w[j], div_q_f32<Codes<IBITS>::kQmax>(m[j]), acc, bad);
+    double mx = 0.0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) mx = dmax_nn(mx, fabs(acc[i]));
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) mx = dmax_nn(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+    if (tl == 0) {
+      absmax[b] = mx;
+      if (!(mx <= DBL_MAX)) raise_flag(flag, FLAG_NONFINITE);
+    }
+    const double inv = mx > 0.0 ? __ddiv_rn((double)QMAX, mx) : 0.0;
+    // r = RN(acc*inv) + 2^52+2^51: its low word is rint-even(acc*inv) (|.| <= qmax,
+    // no clamp needed) and r - (2^52+2^51) is that code as an exact double
+    double r[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) r[i] = __dadd_rn(__dmul_rn(acc[i], inv), kMagic52);
+    if constexpr (std::is_void<FO>::value) {
+      uint32_t q0[8], q1[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        q0[i] = (uint32_t)__double2loint(r[i]);
+        q1[i] = (uint32_t)__double2loint(r[8 + i]);
+      }
+      // inactive lanes hold zeros: they write the zero padding of a partial
+      // last block (zs/quantizer.py:215-217)
+      uint8_t* dst = codes + u * 2 * OBITS;
+      if constexpr (OBITS == 8) {
+        const uint2 a = pack8_int8(q0), c = pack8_int8(q1);
+        *reinterpret_cast<uint4*>(dst) = make_uint4(a.x, a.y, c.x, c.y);
+      } else {
+        *reinterpret_cast<uint2*>(dst) = make_uint2(pack8_int4(q0), pack8_int4(q1));
+      }
+    } else if (active) {
+      // hop 2 to itself: K3's fold of one source, RN(+0.0 + RN(code*s2)) = RN(code*s2)
+      const double s2 = scale_of<OBITS>(mx);
+      double v[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[i] = __dmul_rn(__dsub_rn(r[i], kMagic52), s2);
+      FO* dst = final_out + e0;
+      if constexpr (sizeof(FO) == 4) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          reinterpret_cast<float4*>(dst)[i] = make_float4(from_f64<float>(v[4 * i]), from_f64<float>(v[4 * i + 1]),
+                                                          from_f64<float>(v[4 * i + 2]), from_f64<float>(v[4 * i + 3]));
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) reinterpret_cast<double2*>(dst)[i] = make_double2(v[2 * i], v[2 * i + 1]);
+      }
+    }
+  }
   if (bad) raise_flag(flag, FLAG_BADCODE);
 }
 

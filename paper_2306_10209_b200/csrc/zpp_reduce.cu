@@ -57,9 +57,40 @@ size_t drq_workspace_bytes(int64_t n, int64_t out_block) {
   return (size_t)(ceil_div(n, out_block) * out_block) * sizeof(double);
 }
 
+// fixed fan-in fast path (drq_fast_kernel): fp32 absmax, 512-element output
+// blocks, power-of-two input blocks, 1/2/4/8 sources (the qgZ hop-1 shapes)
+static bool drq_fast_ok(int n_src, int64_t n, int64_t in_block, int64_t out_block, bool a64) {
+  return !a64 && out_block == 512 && n % 16 == 0 && in_block % 16 == 0 &&
+         (in_block & (in_block - 1)) == 0 && (n_src == 1 || n_src == 2 || n_src == 4 || n_src == 8);
+}
+
+template <int IBITS, int OBITS, typename FO>
+static int run_drq_fast(const SrcTable& t, int n_src, int64_t n, int64_t in_block, int64_t nbo, uint8_t* codes,
+                        double* absmax, FO* final_out, uint32_t* flag, cudaStream_t st) {
+  const int lg1 = __builtin_ctzll((unsigned long long)in_block);
+#define ZPP_FAST(NS)                                                                            \
+  {                                                                                             \
+    auto k = drq_fast_kernel<IBITS, OBITS, NS, FO>;                                             \
+    const int grid = grid_for(k, 256, ceil_div(nbo, 8));                                        \
+    k<<<grid, 256, 0, st>>>(t, n, lg1, nbo, codes, absmax, flag, final_out);                    \
+    return check_cuda(cudaGetLastError(), "drq_fast_kernel launch");                            \
+  }
+  switch (n_src) {
+    case 1: ZPP_FAST(1)
+    case 2: ZPP_FAST(2)
+    case 4: ZPP_FAST(4)
+    case 8: ZPP_FAST(8)
+  }
+#undef ZPP_FAST
+  return fail(ZPP_ERR_VALIDATION, "no fast K2 for this fan-in");
+}
+
 template <int IBITS, typename IA, int OBITS, int LANES>
 static int run_drq(const SrcTable& t, int n_src, int64_t n, int64_t in_block, int64_t nbo, uint8_t* codes,
                    double* absmax, bool validate, uint32_t* flag, cudaStream_t st) {
+  if (LANES == 32 && drq_fast_ok(n_src, n, in_block, 512, sizeof(IA) == 8) &&
+      codes_aligned(t, n_src, IBITS))
+    return run_drq_fast<IBITS, OBITS, void>(t, n_src, n, in_block, nbo, codes, absmax, nullptr, flag, st);
   if (n % 16 == 0 && in_block % 16 == 0 && codes_aligned(t, n_src, IBITS)) {
     auto k = validate ? drq16_kernel<IBITS, IA, OBITS, LANES, true> : drq16_kernel<IBITS, IA, OBITS, LANES, false>;
     const int grid = grid_for(k, 256, ceil_div(nbo, 256 / LANES));
@@ -144,6 +175,11 @@ int launch_drq_final(const void* const* codes, const void* const* absmax, int ab
   const bool a64 = absmax_dtype == ZPP_F64;
 #define ZPP_F(IB, IA, OB, FO)                                                                         \
   {                                                                                                   \
+    if (drq_fast_ok(n_src, n, in_block, out_block, a64)) {                                     \
+      *handled = true;                                                                                \
+      return run_drq_fast<IB, OB, FO>(t, n_src, n, in_block, nbo, nullptr, out_absmax,                \
+                                      reinterpret_cast<FO*>(out), flag, st);                          \
+    }                                                                                                 \
     auto k = drq16_kernel<IB, IA, OB, 32, false, FO>;                                                 \
     const int grid = grid_for(k, 256, ceil_div(nbo, 8));                                              \
     k<<<grid, 256, 0, st>>>(t, n_src, n, in_block, nbo, nullptr, out_absmax, flag,                    \

@@ -364,3 +364,37 @@ def test_dequant_reduce_many_sources(n_src, bits, block, n):
     for dt in ("fp32", "fp16", "bf16"):
         got = zpp.dequant_reduce(qs, getattr(torch, {"fp32": "float32", "fp16": "float16", "bf16": "bfloat16"}[dt]))
         assert np.array_equal(got.double().cpu().numpy(), gu.round_to(acc, dt)), dt
+
+
+@pytest.mark.parametrize("n_src", [1, 2, 4, 8])
+def test_fused_fixed_fanin_fast_path(n_src):
+    """K2 fixed fan-in kernel (drq_fast_kernel: 1/2/4/8 sources, 512-element
+    output blocks, power-of-two input blocks): codes and f64 scales bit-exact
+    vs the oracle's fused_dequant_reduce_quant (zs/quantizer.py:241-258),
+    including a partial last output block and bf16-sourced exact ties; a
+    -8 / -128 code raises IntegrityError like the reference's dequantize."""
+    zpp = _zpp()
+    g = torch.Generator(device="cpu").manual_seed(50 + n_src)
+    for n in (4096 + 512 + 48, 8192):
+        for ib in (16, 64, 512, 2048):
+            for ibits, obits in ((4, 4), (8, 4), (4, 8), (8, 8)):
+                src_dt = torch.bfloat16 if (ib + ibits) % 3 == 0 else torch.float32
+                vals = [(torch.randn(n, generator=g) * float(2 ** (k % 5 - 2))).to(src_dt) for k in range(n_src)]
+                icfg = zpp.QuantConfig(bit_width=ibits, block_size=ib)
+                ocfg = zpp.QuantConfig(bit_width=obits, block_size=512)
+                qs = [zpp.quantize(v.cuda(), icfg) for v in vals]
+                f = zpp.fused_dequant_reduce_quant(qs, ocfg)
+                ins = []
+                for v in vals:
+                    c, s, _ = O.quantize(v.double().numpy(), ibits, ib)
+                    ins.append((c, s, n, ibits, ib))
+                c, s, _ = O.fused_dequant_reduce_quant(ins, obits, 512)
+                key = (n, ib, ibits, obits, src_dt)
+                assert np.array_equal(f.codes.cpu().numpy(), c), key
+                assert np.array_equal(f.scales.cpu().numpy(), s), key
+    # an invalid code in the last source
+    icfg = zpp.QuantConfig(bit_width=4, block_size=512)
+    qs = [zpp.quantize(torch.randn(4096).cuda(), icfg) for _ in range(n_src)]
+    qs[-1].codes[100] = 0x88  # two -8 nibbles
+    with pytest.raises(zpp.IntegrityError):
+        zpp.fused_dequant_reduce_quant(qs, zpp.QuantConfig(bit_width=4, block_size=512))
