@@ -134,6 +134,14 @@ size_t zpp_comm_sym_bytes(zpp_comm_t comm);
  * (same local index in every group).  Bounded spin (timeout_ms). */
 int zpp_comm_barrier(zpp_comm_t comm, int scope, int timeout_ms, void* errflag, void* stream);
 int zpp_comm_destroy(zpp_comm_t comm);
+/* Stage tracer (diagnostics; not in the reference): while enabled, each qwZ /
+ * qgZ call records timing events on its stream after every launch.
+ * zpp_comm_trace_read waits for the last call's events and writes, per event,
+ * the stage that had just finished (0 begin, 1 quantize, 2 barrier, 3 gather,
+ * 4 K1, 5 K2, 6 K3) and the ms since the call began; returns the event count,
+ * or -status on error. */
+int zpp_comm_trace(zpp_comm_t comm, int enable);
+int zpp_comm_trace_read(zpp_comm_t comm, int* ids, float* ms, int max);
 
 /* qwZ all-gather, fused over NVLink (zs/collectives.py:244-282):
  * quantize this rank's shard into the symmetric buffer, world barrier, then

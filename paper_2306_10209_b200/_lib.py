@@ -50,6 +50,8 @@ SIGNATURES = {
     "zpp_comm_sym_bytes": (c_size_t, [P]),
     "zpp_comm_barrier": (c_int, [P, c_int, c_int, P, P]),
     "zpp_comm_destroy": (c_int, [P]),
+    "zpp_comm_trace": (c_int, [P, c_int]),
+    "zpp_comm_trace_read": (c_int, [P, P, P, c_int]),
     "zpp_qwz_allgather": (c_int, [P, c_size_t, P, c_int, c_int64, c_int, c_int64, P, c_int, c_int64, P, c_int64,
                                   c_int64, P, P]),
     "zpp_hpz_allgather": (c_int, [P, c_size_t, c_int64, c_int, P, P, P]),

@@ -141,6 +141,8 @@ gather_copy_tma_kernel(SrcTable src, int n_src, int rot, int64_t seg_bytes, uint
 
 }  // namespace
 
+static const int kTraceMax = 32;
+
 struct zpp_comm {
   int rank = 0, world = 1, group = 1;
   size_t sym_bytes = 0;
@@ -156,6 +158,12 @@ struct zpp_comm {
   // s run on the caller's stream
   cudaStream_t side = nullptr;
   cudaEvent_t ev_start = nullptr, ev_k1 = nullptr, ev_bar = nullptr;
+  // stage tracer (zpp_comm_trace): timing events between the launches of the
+  // last traced collective, on its stream
+  bool trace = false;
+  int tr_n = 0;
+  int tr_id[kTraceMax] = {};
+  cudaEvent_t tr_ev[kTraceMax] = {};
 
   uint32_t* flag_slot(int owner, int scope, int writer) {
     return reinterpret_cast<uint32_t*>(peers[owner] + sym_bytes) + scope * kMaxRanks + writer;
@@ -194,6 +202,16 @@ static int barrier(zpp_comm_t c, int scope, int timeout_ms, uint32_t* flag, cuda
   const uint64_t to = (uint64_t)(timeout_ms > 0 ? timeout_ms : 60000) * 1000000ull;
   barrier_kernel<<<1, 64, 0, st>>>(a, (int)m.size(), e, to, flag);
   return check_cuda(cudaGetLastError(), "barrier_kernel launch");
+}
+
+// stage ids for the tracer: what just finished when the event was recorded
+enum TraceId { TR_BEGIN = 0, TR_QUANT = 1, TR_BARRIER = 2, TR_GATHER = 3, TR_K1 = 4, TR_K2 = 5, TR_K3 = 6 };
+static void trace_reset(zpp_comm_t c) { c->tr_n = 0; }
+static void trace_mark(zpp_comm_t c, int id, cudaStream_t st) {
+  if (!c->trace || c->tr_n >= kTraceMax) return;
+  if (!c->tr_ev[c->tr_n]) cudaEventCreate(&c->tr_ev[c->tr_n]);
+  c->tr_id[c->tr_n] = id;
+  cudaEventRecord(c->tr_ev[c->tr_n++], st);
 }
 
 static size_t absmax_elem(int dtype) { return dtype == ZPP_F64 ? 8 : 4; }
@@ -275,6 +293,8 @@ int zpp_comm_destroy(zpp_comm_t c) {
     cudaEventDestroy(c->ev_bar);
     cudaStreamDestroy(c->side);
   }
+  for (int i = 0; i < kTraceMax; ++i)
+    if (c->tr_ev[i]) cudaEventDestroy(c->tr_ev[i]);
   for (int r = 0; r < c->world; ++r)
     if (c->opened[r]) cudaIpcCloseMemHandle(c->peers[r]);
   cudaFree(c->local);
@@ -307,6 +327,8 @@ int zpp_qwz_allgather(zpp_comm_t c, size_t sym_offset, const void* shard, int dt
   const size_t region = qwz_region(shard_len, bits, block, ZPP_F64);
   if (sym_offset + 2 * region > c->sym_bytes) return fail(ZPP_ERR_VALIDATION, "symmetric buffer too small for qwZ");
   if (shard_len == 0) return ZPP_OK;
+  trace_reset(c);
+  trace_mark(c, TR_BEGIN, reinterpret_cast<cudaStream_t>(stream));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   uint32_t* flag = reinterpret_cast<uint32_t*>(errflag);
   const size_t base = sym_offset + (c->qwz_uses++ & 1) * region;
@@ -323,16 +345,20 @@ int zpp_qwz_allgather(zpp_comm_t c, size_t sym_offset, const void* shard, int dt
   rc = launch_quantize(shard, dtype, a, shard_len, bits, block, c->local + base,
                        c->local + base + abs_off, flag, st);
   if (rc) return rc;
+  trace_mark(c, TR_QUANT, st);
   rc = barrier(c, 0, kBarrierTimeoutMs, flag, st);
   if (rc) return rc;
+  trace_mark(c, TR_BARRIER, st);
   const void* codes[kMaxRanks];
   const void* absmax[kMaxRanks];
   for (int r = 0; r < c->world; ++r) {
     codes[r] = c->peers[r] + base;
     absmax[r] = c->peers[r] + base + abs_off;
   }
-  return launch_gather_dequant(codes, absmax, dtype == ZPP_F64 ? ZPP_F64 : ZPP_F32, c->world, c->rank, shard_len,
-                               bits, block, out, out_dtype, sec_out, sec_lo, sec_len, flag, st, out_stride);
+  rc = launch_gather_dequant(codes, absmax, dtype == ZPP_F64 ? ZPP_F64 : ZPP_F32, c->world, c->rank, shard_len,
+                             bits, block, out, out_dtype, sec_out, sec_lo, sec_len, flag, st, out_stride);
+  trace_mark(c, TR_GATHER, st);
+  return rc;
 }
 
 // ---------------------------------------------------------------------------
@@ -445,6 +471,8 @@ int zpp_qgz_reduce_scatter(zpp_comm_t c, size_t sym_offset, const void* grad, in
     if ((rc = barrier(c, 0, kBarrierTimeoutMs, flag, st))) return rc;
   }
   c->qgz_region = l.region;
+  trace_reset(c);
+  trace_mark(c, TR_BEGIN, st);
   const uint64_t use0 = c->qgz_uses;
   c->qgz_uses += stages;
   auto base_of = [&](int s) { return sym_offset + ((use0 + s) & 1) * l.region; };
@@ -485,8 +513,10 @@ int zpp_qgz_reduce_scatter(zpp_comm_t c, size_t sym_offset, const void* grad, in
     } else if ((rc = k1(s, st))) {
       return rc;
     }
+    trace_mark(c, TR_K1, st);
     rc = barrier(c, 1, kBarrierTimeoutMs, flag, st);
     if (rc) return rc;
+    trace_mark(c, TR_BARRIER, st);
     if (pipelined && s + 1 < stages) {
       if ((rc = check_cuda(cudaEventRecord(c->ev_bar, st), "record"))) return rc;
       if ((rc = check_cuda(cudaStreamWaitEvent(c->side, c->ev_bar, 0), "wait"))) return rc;
@@ -504,31 +534,80 @@ int zpp_qgz_reduce_scatter(zpp_comm_t c, size_t sym_offset, const void* grad, in
     }
     if (Y == 1) {  // hop 2 is a self-send: K2 writes the final partition directly
       bool handled = false;
+      if (in_abs == ZPP_F32)
+        rc = launch_drq_tma(codes, absmax, X, msg_elems, intra_bits, intra_block, inter_bits, inter_block, nullptr,
+                            reinterpret_cast<double*>(c->local + base + l.hop_abs),
+                            reinterpret_cast<uint8_t*>(out) + (size_t)s * L * out_esz, out_dtype, flag, st, &handled);
+      if (rc) return rc;
+      if (handled) {
+        trace_mark(c, TR_K2, st);
+        continue;
+      }
       rc = launch_drq_final(codes, absmax, in_abs, X, msg_elems, intra_bits, intra_block, inter_bits, inter_block,
                             reinterpret_cast<double*>(c->local + base + l.hop_abs),
                             reinterpret_cast<uint8_t*>(out) + (size_t)s * L * out_esz, out_dtype, flag, st, &handled);
       if (rc) return rc;
-      if (handled) continue;
+      if (handled) {
+        trace_mark(c, TR_K2, st);
+        continue;
+      }
     }
-    rc = launch_drq(codes, absmax, in_abs, X, msg_elems, intra_bits, intra_block, inter_bits, inter_block,
-                    c->local + base + l.hop_codes, reinterpret_cast<double*>(c->local + base + l.hop_abs),
-                    c->local + base + l.ws, drq_workspace_bytes(msg_elems, inter_block), flag, st,
-                    /*validate=*/false);
+    bool handled = false;
+    if (in_abs == ZPP_F32)
+      rc = launch_drq_tma(codes, absmax, X, msg_elems, intra_bits, intra_block, inter_bits, inter_block,
+                          c->local + base + l.hop_codes, reinterpret_cast<double*>(c->local + base + l.hop_abs),
+                          nullptr, 0, flag, st, &handled);
     if (rc) return rc;
+    if (!handled)
+      rc = launch_drq(codes, absmax, in_abs, X, msg_elems, intra_bits, intra_block, inter_bits, inter_block,
+                      c->local + base + l.hop_codes, reinterpret_cast<double*>(c->local + base + l.hop_abs),
+                      c->local + base + l.ws, drq_workspace_bytes(msg_elems, inter_block), flag, st,
+                      /*validate=*/false);
+    if (rc) return rc;
+    trace_mark(c, TR_K2, st);
     rc = barrier(c, 2, kBarrierTimeoutMs, flag, st);
     if (rc) return rc;
+    trace_mark(c, TR_BARRIER, st);
     // K3: pull segment `node` from the rank with my local index in every group
     for (int g = 0; g < Y; ++g) {
       const uint8_t* p = c->peers[g * X + loc] + base;
       codes[g] = p + l.hop_codes + (size_t)code_bytes(L, inter_bits, inter_block) * node;
       absmax[g] = p + l.hop_abs + (size_t)(L / inter_block) * 8 * node;
     }
-    rc = launch_dequant_reduce(codes, absmax, ZPP_F64, Y, L, inter_bits, inter_block,
-                               reinterpret_cast<uint8_t*>(out) + (size_t)s * L * out_esz, out_dtype, 1.0, flag, st,
-                               /*validate=*/false);
+    handled = false;
+    rc = launch_dr_tma(codes, absmax, Y, L, inter_bits, inter_block,
+                       reinterpret_cast<uint8_t*>(out) + (size_t)s * L * out_esz, out_dtype, flag, st, &handled);
     if (rc) return rc;
+    if (!handled)
+      rc = launch_dequant_reduce(codes, absmax, ZPP_F64, Y, L, inter_bits, inter_block,
+                                 reinterpret_cast<uint8_t*>(out) + (size_t)s * L * out_esz, out_dtype, 1.0, flag,
+                                 st, /*validate=*/false);
+    if (rc) return rc;
+    trace_mark(c, TR_K3, st);
   }
   return ZPP_OK;
+}
+
+int zpp_comm_trace(zpp_comm_t c, int enable) {
+  if (!c) return fail(ZPP_ERR_VALIDATION, "null communicator");
+  c->trace = enable != 0;
+  c->tr_n = 0;
+  return ZPP_OK;
+}
+
+int zpp_comm_trace_read(zpp_comm_t c, int* ids, float* ms, int max) {
+  if (!c || (max > 0 && (!ids || !ms))) return fail(ZPP_ERR_VALIDATION, "bad arguments");
+  const int n = c->tr_n < max ? c->tr_n : max;
+  if (n == 0) return 0;
+  int rc = check_cuda(cudaEventSynchronize(c->tr_ev[n - 1]), "trace sync");
+  if (rc) return -rc;
+  for (int i = 0; i < n; ++i) {
+    ids[i] = c->tr_id[i];
+    ms[i] = 0.0f;
+    if (i > 0 && (rc = check_cuda(cudaEventElapsedTime(&ms[i], c->tr_ev[0], c->tr_ev[i]), "trace elapsed")))
+      return -rc;
+  }
+  return n;
 }
 
 }  // extern "C"

@@ -42,6 +42,14 @@ int launch_drq(const void* const* codes, const void* const* absmax, int absmax_d
 int launch_drq_final(const void* const* codes, const void* const* absmax, int absmax_dtype, int n_src, int64_t n,
                      int in_bits, int64_t in_block, int out_bits, int64_t out_block, double* out_absmax, void* out,
                      int out_dtype, uint32_t* flag, cudaStream_t st, bool* handled);
+// TMA-fed K2 / K3 for the communicator's qgZ hops (sources in symmetric,
+// 256-byte padded regions).  *handled = false when the shape has no TMA path.
+// final_out != nullptr: K2 writes the final partition (hop 2 is a self-send).
+int launch_drq_tma(const void* const* codes, const void* const* absmax, int n_src, int64_t n, int in_bits,
+                   int64_t in_block, int out_bits, int64_t out_block, uint8_t* out_codes, double* out_absmax,
+                   void* final_out, int final_dtype, uint32_t* flag, cudaStream_t st, bool* handled);
+int launch_dr_tma(const void* const* codes, const void* const* absmax_f64, int n_src, int64_t n, int bits,
+                  int64_t block, void* out, int out_dtype, uint32_t* flag, cudaStream_t st, bool* handled);
 size_t drq_workspace_bytes(int64_t n, int64_t out_block);
 bool drq_has_reg_path(int64_t out_block);
 

@@ -1377,23 +1377,37 @@ drq_fast_kernel(SrcTable src, int64_t n, int lg1, int64_t n_blocks_out, uint8_t*
   const int tl = threadIdx.x & 31;
   const int64_t nwarp = ((int64_t)gridDim.x * blockDim.x) >> 5;
   bool bad = false;
-  for (int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < n_blocks_out; b += nwarp) {
+  // the sources live in peers' HBM (NVLink): the next block's codes and absmax
+  // are loaded before this block is folded (register double buffer), so each
+  // warp keeps its loads in flight across the compute
+  V w[NSRC], wn[NSRC];
+  float m[NSRC], mn[NSRC];
+  auto load = [&](int64_t b, V (&wv)[NSRC], float (&mv)[NSRC]) {
+    const int64_t e0 = b * 512 + (int64_t)tl * 16;
+    const bool ok = b < n_blocks_out && e0 < n;
+#pragma unroll
+    for (int j = 0; j < NSRC; ++j) {
+      if (ok) {
+        wv[j] = __ldg(reinterpret_cast<const V*>(src.codes[j]) + (e0 >> 4));
+        mv[j] = __ldg(reinterpret_cast<const float*>(src.absmax[j]) + (e0 >> lg1));
+      } else {
+        wv[j] = V{};
+        mv[j] = 0.0f;
+      }
+    }
+  };
+  int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  load(b, wn, mn);
+  for (; b < n_blocks_out; b += nwarp) {
     const int64_t e0 = b * 512 + (int64_t)tl * 16;
     const bool active = e0 < n;  // n % 16 == 0: lanes are all-valid or all-empty
     const int64_t u = e0 >> 4;
-    const int64_t ib = e0 >> lg1;
-    V w[NSRC];
-    float m[NSRC];
 #pragma unroll
     for (int j = 0; j < NSRC; ++j) {
-      if (active) {
-        w[j] = __ldg(reinterpret_cast<const V*>(src.codes[j]) + u);
-        m[j] = __ldg(reinterpret_cast<const float*>(src.absmax[j]) + ib);
-      } else {
-        w[j] = V{};
-        m[j] = 0.0f;
-      }
+      w[j] = wn[j];
+      m[j] = mn[j];
     }
+    load(b + nwarp, wn, mn);
     double acc[16];
     fold16<IBITS, true, true>(w[0], div_q_f32<Codes<IBITS>::kQmax>(m[0]), acc, bad);
 #pragma unroll
@@ -1446,6 +1460,290 @@ drq_fast_kernel(SrcTable src, int64_t n, int lg1, int64_t n_blocks_out, uint8_t*
         for (int i = 0; i < 8; ++i) reinterpret_cast<double2*>(dst)[i] = make_double2(v[2 * i], v[2 * i + 1]);
       }
     }
+  }
+  if (bad) raise_flag(flag, FLAG_BADCODE);
+}
+
+// K3 fixed fan-in fast path (the qgZ hop-2 fold, zs/collectives.py:536-544):
+// NSRC sources known at compile time, power-of-two block, fp32/f64 output;
+// lane = 16 contiguous elements, grid-stride, next unit's codes and absmax
+// loaded before this unit is folded (the sources are peers' HBM).  The first
+// source assigns (see fold16).  Same arithmetic as dr_unit.
+template <int BITS, int NSRC, typename A, typename O>
+__global__ void __launch_bounds__(256)
+dr_fast_kernel(SrcTable src, int64_t n, int lg, O* __restrict__ out, double post_scale, uint32_t* __restrict__ flag) {
+  using V = typename Vec16<BITS>::T;
+  const int64_t units = n / 16;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  bool bad = false;
+  V w[NSRC], wn[NSRC];
+  A m[NSRC], mn[NSRC];
+  auto load = [&](int64_t u, V (&wv)[NSRC], A (&mv)[NSRC]) {
+#pragma unroll
+    for (int j = 0; j < NSRC; ++j) {
+      if (u < units) {
+        wv[j] = __ldg(reinterpret_cast<const V*>(src.codes[j]) + u);
+        mv[j] = __ldg(reinterpret_cast<const A*>(src.absmax[j]) + ((u * 16) >> lg));
+      } else {
+        wv[j] = V{};
+        mv[j] = A(0);
+      }
+    }
+  };
+  int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  load(u, wn, mn);
+  for (; u < units; u += stride) {
+#pragma unroll
+    for (int j = 0; j < NSRC; ++j) {
+      w[j] = wn[j];
+      m[j] = mn[j];
+    }
+    load(u + stride, wn, mn);
+    double acc[16];
+    fold16<BITS, true, true>(w[0], scale_of<BITS>((double)m[0]), acc, bad);
+#pragma unroll
+    for (int j = 1; j < NSRC; ++j) fold16<BITS, true>(w[j], scale_of<BITS>((double)m[j]), acc, bad);
+    if (post_scale != 1.0) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) acc[i] = __dmul_rn(acc[i], post_scale);
+    }
+    O* dst = out + u * 16;
+    if constexpr (sizeof(O) == 4) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        reinterpret_cast<float4*>(dst)[i] = make_float4(from_f64<float>(acc[4 * i]), from_f64<float>(acc[4 * i + 1]),
+                                                        from_f64<float>(acc[4 * i + 2]), from_f64<float>(acc[4 * i + 3]));
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) reinterpret_cast<double2*>(dst)[i] = make_double2(acc[2 * i], acc[2 * i + 1]);
+    }
+  }
+  if (bad) raise_flag(flag, FLAG_BADCODE);
+}
+
+// ---------------------------------------------------------------------------
+// K2 / K3 fed by TMA (the multi-GPU qgZ hops).  Their sources are slices of
+// peers' symmetric buffers: plain per-thread loads over NVLink stall at a few
+// hundred GB/s, so one elected thread streams each tile's codes and absmax of
+// every source with cp.async.bulk into a STAGES-deep shared ring (mbarrier
+// transaction counts), and all 256 threads fold from shared memory.  A tile
+// is `tu` 16-element units of every source.  Bulk copies need 16-byte aligned
+// addresses and sizes, so each absmax slice is widened to 16-byte bounds and
+// the last codes slice rounded up: the host only uses these kernels on the
+// communicator's symmetric regions, which are padded to 256 bytes.
+
+struct TmaTile {
+  int tu;             // units (16 elements) per tile
+  int lg;             // log2 of the input block size
+  int code_slot;      // bytes per source codes slot (16-aligned)
+  int abs_slot;       // bytes per source absmax slot (16-aligned)
+  int stage_bytes;    // NSRC * (code_slot + abs_slot)
+};
+
+template <int BITS, int NSRC, typename A>
+__device__ __forceinline__ void tma_issue_tile(const SrcTable& src, const TmaTile& tt, int64_t units, int64_t t,
+                                               uint8_t* stage, uint64_t* bar) {
+  constexpr int UB = 2 * BITS;  // bytes per unit of codes
+  const int64_t u0 = t * tt.tu;
+  const int64_t nu = min((int64_t)tt.tu, units - u0);
+  const uint32_t cbytes = (uint32_t)((nu * UB + 15) & ~15);
+  const int64_t b_first = (u0 * 16) >> tt.lg, b_last = ((u0 + nu) * 16 - 1) >> tt.lg;
+  uint32_t total = 0;
+#pragma unroll
+  for (int j = 0; j < NSRC; ++j) {
+    const uintptr_t a0 = reinterpret_cast<uintptr_t>(src.absmax[j]) + (uintptr_t)b_first * sizeof(A);
+    const uintptr_t a1 = reinterpret_cast<uintptr_t>(src.absmax[j]) + (uintptr_t)(b_last + 1) * sizeof(A);
+    total += cbytes + (uint32_t)(((a1 + 15) & ~(uintptr_t)15) - (a0 & ~(uintptr_t)15));
+  }
+  mbar_expect_tx(bar, total);
+#pragma unroll
+  for (int j = 0; j < NSRC; ++j) {
+    uint8_t* slot = stage + j * (tt.code_slot + tt.abs_slot);
+    bulk_g2s(slot, src.codes[j] + u0 * UB, cbytes, bar);
+    const uintptr_t a0 = reinterpret_cast<uintptr_t>(src.absmax[j]) + (uintptr_t)b_first * sizeof(A);
+    const uintptr_t a1 = reinterpret_cast<uintptr_t>(src.absmax[j]) + (uintptr_t)(b_last + 1) * sizeof(A);
+    const uintptr_t lo = a0 & ~(uintptr_t)15;
+    bulk_g2s(slot + tt.code_slot, reinterpret_cast<const void*>(lo), (uint32_t)(((a1 + 15) & ~(uintptr_t)15) - lo), bar);
+  }
+}
+
+// absmax of input block b (first block of tile: b_first) of source j in a stage
+template <typename A>
+__device__ __forceinline__ double tma_absmax(const SrcTable& src, int j, const uint8_t* slot_abs, int64_t b_first,
+                                             int64_t b) {
+  const uintptr_t a0 = reinterpret_cast<uintptr_t>(src.absmax[j]) + (uintptr_t)b_first * sizeof(A);
+  const int skew = (int)(a0 & 15);
+  return (double)*reinterpret_cast<const A*>(slot_abs + skew + (b - b_first) * sizeof(A));
+}
+
+// K2 (hop-1 fold + requant into 512-element blocks, or the final partition
+// when hop 2 is a self-send): fp32 absmax sources, warp = output block.
+template <int IBITS, int OBITS, int NSRC, typename FO, int STAGES>
+__global__ void __launch_bounds__(256)
+drq_tma_kernel(SrcTable src, int64_t n, TmaTile tt, uint8_t* __restrict__ codes, double* __restrict__ absmax,
+               uint32_t* __restrict__ flag, FO* __restrict__ final_out) {
+  using V = typename Vec16<IBITS>::T;
+  constexpr int UB = 2 * IBITS;
+  constexpr int QMAX = Codes<OBITS>::kQmax;
+  extern __shared__ __align__(128) uint8_t dsm[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(dsm + (size_t)STAGES * tt.stage_bytes);
+  const int tid = threadIdx.x, tl = tid & 31, wid = tid >> 5;
+  const int64_t units = n / 16;
+  const int64_t tiles = (units + tt.tu - 1) / tt.tu;
+  const int64_t G = gridDim.x;
+  if (tid == 0) {
+#pragma unroll
+    for (int i = 0; i < STAGES; ++i) mbar_init(&full[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0) {
+#pragma unroll
+    for (int k = 0; k < STAGES - 1; ++k)
+      if (blockIdx.x + k * G < tiles)
+        tma_issue_tile<IBITS, NSRC, float>(src, tt, units, blockIdx.x + k * G, dsm + (size_t)k * tt.stage_bytes,
+                                           &full[k]);
+  }
+  bool bad = false;
+  int k = 0;
+  for (int64_t t = blockIdx.x; t < tiles; t += G, ++k) {
+    const int slot = k % STAGES;
+    if (tid == 0) {
+      const int64_t tn = t + (STAGES - 1) * G;
+      const int sn = (k + STAGES - 1) % STAGES;
+      if (tn < tiles) tma_issue_tile<IBITS, NSRC, float>(src, tt, units, tn, dsm + (size_t)sn * tt.stage_bytes, &full[sn]);
+    }
+    mbar_wait(&full[slot], (uint32_t)((k / STAGES) & 1));
+    const uint8_t* stage = dsm + (size_t)slot * tt.stage_bytes;
+    const int64_t u0 = t * tt.tu;
+    const int64_t b_first = (u0 * 16) >> tt.lg;
+    for (int ob = wid; ob < tt.tu / 32; ob += 8) {  // output block = 32 units
+      const int lu = ob * 32 + tl;
+      const int64_t unit = u0 + lu;
+      const bool active = unit < units;
+      if (u0 + ob * 32 >= units) break;  // warp-uniform: block entirely past the end
+      double acc[16];
+#pragma unroll
+      for (int j = 0; j < NSRC; ++j) {
+        const uint8_t* sl = stage + j * (tt.code_slot + tt.abs_slot);
+        V w = active ? *reinterpret_cast<const V*>(sl + lu * UB) : V{};
+        const double m = active ? tma_absmax<float>(src, j, sl + tt.code_slot, b_first, (unit * 16) >> tt.lg) : 0.0;
+        const double sc = div_q_f32<Codes<IBITS>::kQmax>((float)m);
+        if (j == 0) fold16<IBITS, true, true>(w, sc, acc, bad);
+        else fold16<IBITS, true>(w, sc, acc, bad);
+      }
+      double mx = 0.0;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) mx = dmax_nn(mx, fabs(acc[i]));
+#pragma unroll
+      for (int off = 16; off >= 1; off >>= 1) mx = dmax_nn(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+      const int64_t bo = (u0 + ob * 32) / 32;  // output block index
+      if (tl == 0) {
+        absmax[bo] = mx;
+        if (!(mx <= DBL_MAX)) raise_flag(flag, FLAG_NONFINITE);
+      }
+      const double inv = mx > 0.0 ? __ddiv_rn((double)QMAX, mx) : 0.0;
+      double r[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) r[i] = __dadd_rn(__dmul_rn(acc[i], inv), kMagic52);
+      if constexpr (std::is_void<FO>::value) {
+        uint32_t q0[8], q1[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          q0[i] = (uint32_t)__double2loint(r[i]);
+          q1[i] = (uint32_t)__double2loint(r[8 + i]);
+        }
+        uint8_t* dst = codes + unit * 2 * OBITS;  // inactive lanes: zero padding
+        if constexpr (OBITS == 8) {
+          const uint2 a = pack8_int8(q0), c = pack8_int8(q1);
+          *reinterpret_cast<uint4*>(dst) = make_uint4(a.x, a.y, c.x, c.y);
+        } else {
+          *reinterpret_cast<uint2*>(dst) = make_uint2(pack8_int4(q0), pack8_int4(q1));
+        }
+      } else if (active) {
+        const double s2 = scale_of<OBITS>(mx);
+        double v[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = __dmul_rn(__dsub_rn(r[i], kMagic52), s2);
+        FO* dst = final_out + unit * 16;
+        if constexpr (sizeof(FO) == 4) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            reinterpret_cast<float4*>(dst)[i] = make_float4(from_f64<float>(v[4 * i]), from_f64<float>(v[4 * i + 1]),
+                                                            from_f64<float>(v[4 * i + 2]), from_f64<float>(v[4 * i + 3]));
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) reinterpret_cast<double2*>(dst)[i] = make_double2(v[2 * i], v[2 * i + 1]);
+        }
+      }
+    }
+    __syncthreads();  // every thread is done with this slot before it is refilled
+  }
+  if (bad) raise_flag(flag, FLAG_BADCODE);
+}
+
+// K3 (hop-2 fold into the rank's partition): f64 absmax sources from K2.
+template <int BITS, int NSRC, typename O, int STAGES>
+__global__ void __launch_bounds__(256)
+dr_tma_kernel(SrcTable src, int64_t n, TmaTile tt, O* __restrict__ out, uint32_t* __restrict__ flag) {
+  using V = typename Vec16<BITS>::T;
+  constexpr int UB = 2 * BITS;
+  extern __shared__ __align__(128) uint8_t dsm[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(dsm + (size_t)STAGES * tt.stage_bytes);
+  const int tid = threadIdx.x;
+  const int64_t units = n / 16;
+  const int64_t tiles = (units + tt.tu - 1) / tt.tu;
+  const int64_t G = gridDim.x;
+  if (tid == 0) {
+#pragma unroll
+    for (int i = 0; i < STAGES; ++i) mbar_init(&full[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0) {
+#pragma unroll
+    for (int k = 0; k < STAGES - 1; ++k)
+      if (blockIdx.x + k * G < tiles)
+        tma_issue_tile<BITS, NSRC, double>(src, tt, units, blockIdx.x + k * G, dsm + (size_t)k * tt.stage_bytes,
+                                           &full[k]);
+  }
+  bool bad = false;
+  int k = 0;
+  for (int64_t t = blockIdx.x; t < tiles; t += G, ++k) {
+    const int slot = k % STAGES;
+    if (tid == 0) {
+      const int64_t tn = t + (STAGES - 1) * G;
+      const int sn = (k + STAGES - 1) % STAGES;
+      if (tn < tiles) tma_issue_tile<BITS, NSRC, double>(src, tt, units, tn, dsm + (size_t)sn * tt.stage_bytes, &full[sn]);
+    }
+    mbar_wait(&full[slot], (uint32_t)((k / STAGES) & 1));
+    const uint8_t* stage = dsm + (size_t)slot * tt.stage_bytes;
+    const int64_t u0 = t * tt.tu;
+    const int64_t b_first = (u0 * 16) >> tt.lg;
+    for (int lu = tid; lu < tt.tu; lu += 256) {
+      const int64_t unit = u0 + lu;
+      if (unit >= units) break;
+      double acc[16];
+#pragma unroll
+      for (int j = 0; j < NSRC; ++j) {
+        const uint8_t* sl = stage + j * (tt.code_slot + tt.abs_slot);
+        const V w = *reinterpret_cast<const V*>(sl + lu * UB);
+        const double sc = scale_of<BITS>(tma_absmax<double>(src, j, sl + tt.code_slot, b_first, (unit * 16) >> tt.lg));
+        if (j == 0) fold16<BITS, true, true>(w, sc, acc, bad);
+        else fold16<BITS, true>(w, sc, acc, bad);
+      }
+      O* dst = out + unit * 16;
+      if constexpr (sizeof(O) == 4) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          reinterpret_cast<float4*>(dst)[i] = make_float4(from_f64<float>(acc[4 * i]), from_f64<float>(acc[4 * i + 1]),
+                                                          from_f64<float>(acc[4 * i + 2]), from_f64<float>(acc[4 * i + 3]));
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) reinterpret_cast<double2*>(dst)[i] = make_double2(acc[2 * i], acc[2 * i + 1]);
+      }
+    }
+    __syncthreads();
   }
   if (bad) raise_flag(flag, FLAG_BADCODE);
 }

@@ -5,11 +5,26 @@
 // general 8-element kernels for odd block sizes and alignments.  `validate`
 // turns the IntegrityError code check on (API calls) or off (internal qgZ hops,
 // whose codes come from this library's own quantizer).
+#include <algorithm>
+#include <cstdlib>
+
 #include "zpp_internal.h"
 #include "zpp_kernels.cuh"
 #include "zpp_launch.cuh"
 
 namespace zpp {
+
+// ZPP_FORCE_TMA=1 (development only): route the public K2/K3 entry points to
+// the TMA-fed kernels so they can be timed on local buffers.  Those kernels
+// may read up to 16 bytes past each source slice, which stays inside torch's
+// 512-byte allocation granules.
+static bool force_tma() {
+  static const bool on = [] {
+    const char* e = getenv("ZPP_FORCE_TMA");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
 
 static bool codes_aligned(const SrcTable& t, int n_src, int bits) {
   for (int i = 0; i < n_src; ++i)
@@ -20,9 +35,31 @@ static bool codes_aligned(const SrcTable& t, int n_src, int bits) {
 // ---------------------------------------------------------------------------
 // K3
 
+// K3 fixed fan-in fast path: 2/4/8 sources, power-of-two block, fp32/f64 out
+template <int BITS, int NS, typename A, typename O>
+static int run_reduce_fast(const SrcTable& t, int64_t n, int lg, void* out, double post_scale, uint32_t* flag,
+                           cudaStream_t st) {
+  auto k = dr_fast_kernel<BITS, NS, A, O>;
+  const int grid = grid_for(k, 256, ceil_div(n / 16, 256));
+  k<<<grid, 256, 0, st>>>(t, n, lg, reinterpret_cast<O*>(out), post_scale, flag);
+  return check_cuda(cudaGetLastError(), "dr_fast_kernel launch");
+}
+
 template <int BITS, typename A, typename O>
 static int run_reduce(const SrcTable& t, int n_src, int64_t n, int64_t block, void* out, double post_scale,
                       bool validate, uint32_t* flag, cudaStream_t st) {
+  if constexpr (sizeof(O) >= 4) {
+    if (n % 16 == 0 && block % 16 == 0 && (block & (block - 1)) == 0 && aligned16(out) &&
+        codes_aligned(t, n_src, BITS)) {
+      const int lg = __builtin_ctzll((unsigned long long)block);
+      switch (n_src) {
+        case 2: return run_reduce_fast<BITS, 2, A, O>(t, n, lg, out, post_scale, flag, st);
+        case 4: return run_reduce_fast<BITS, 4, A, O>(t, n, lg, out, post_scale, flag, st);
+        case 8: return run_reduce_fast<BITS, 8, A, O>(t, n, lg, out, post_scale, flag, st);
+        default: break;
+      }
+    }
+  }
   if (n % 16 == 0 && block % 16 == 0 && aligned16(out) && codes_aligned(t, n_src, BITS)) {
     auto k = validate ? dequant_reduce16_kernel<BITS, A, O, true> : dequant_reduce16_kernel<BITS, A, O, false>;
     const int grid = grid_for(k, 256, ceil_div(n / 16, 256));
@@ -39,6 +76,11 @@ int launch_dequant_reduce(const void* const* codes, const void* const* absmax, i
                           int bits, int64_t block, void* out, int out_dtype, double post_scale, uint32_t* flag,
                           cudaStream_t st, bool validate) {
   if (n == 0) return ZPP_OK;
+  if (force_tma() && absmax_dtype == ZPP_F64 && post_scale == 1.0) {  // development: time the TMA K3 locally
+    bool handled = false;
+    int rc = launch_dr_tma(codes, absmax, n_src, n, bits, block, out, out_dtype, flag, st, &handled);
+    if (rc || handled) return rc;
+  }
   SrcTable t;
   int rc = fill_table(t, codes, absmax, n_src);
   if (rc) return rc;
@@ -130,6 +172,12 @@ int launch_drq(const void* const* codes, const void* const* absmax, int absmax_d
   if (rc) return rc;
   if (absmax_dtype != ZPP_F32 && absmax_dtype != ZPP_F64)
     return fail(ZPP_ERR_VALIDATION, "absmax dtype must be F32 or F64");
+  if (force_tma() && absmax_dtype == ZPP_F32) {  // development: time the TMA K2 locally
+    bool handled = false;
+    rc = launch_drq_tma(codes, absmax, n_src, n, in_bits, in_block, out_bits, out_block, out_codes, out_absmax,
+                        nullptr, 0, flag, st, &handled);
+    if (rc || handled) return rc;
+  }
   const bool a64 = absmax_dtype == ZPP_F64;
   bool aligned = true;  // 8-element chunk loads need 8 B (INT8) / 4 B (INT4) aligned codes
   for (int i = 0; i < n_src; ++i) aligned = aligned && (reinterpret_cast<uintptr_t>(codes[i]) % in_bits) == 0;
@@ -199,6 +247,127 @@ int launch_drq_final(const void* const* codes, const void* const* absmax, int ab
 #undef ZPP_FO
 #undef ZPP_F
   return ZPP_OK;
+}
+
+// ---------------------------------------------------------------------------
+// TMA-fed K2 / K3 (multi-GPU qgZ hops)
+
+static constexpr int kTmaStages = 3;
+
+static TmaTile tma_tile(int n_src, int bits, int64_t block, size_t abs_size) {
+  TmaTile tt;
+  const int ub = 2 * bits;
+  int tu = 4096;
+  while (tu > 32 && (int64_t)n_src * tu * ub > 24576) tu >>= 1;
+  tt.tu = tu;
+  tt.lg = __builtin_ctzll((unsigned long long)block);
+  tt.code_slot = (int)((tu * ub + 15) & ~15);
+  tt.abs_slot = (int)((((int64_t)tu * 16 / block + 2) * (int64_t)abs_size + 32 + 15) & ~15);
+  tt.stage_bytes = n_src * (tt.code_slot + tt.abs_slot);
+  return tt;
+}
+
+template <typename K>
+static int tma_grid(K k, const TmaTile& tt, int64_t tiles, size_t* smem) {
+  *smem = (size_t)kTmaStages * tt.stage_bytes + kTmaStages * 8;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*smem);
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 256, *smem);
+  return (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sm_count() * std::max(occ, 1), tiles));
+}
+
+template <int IB, int OB, int NS, typename FO>
+static int run_drq_tma(const SrcTable& t, int64_t n, int64_t in_block, uint8_t* codes, double* absmax, FO* fo,
+                       uint32_t* flag, cudaStream_t st) {
+  const TmaTile tt = tma_tile(NS, IB, in_block, sizeof(float));
+  auto k = drq_tma_kernel<IB, OB, NS, FO, kTmaStages>;
+  size_t smem = 0;
+  const int grid = tma_grid(k, tt, ceil_div(n / 16, tt.tu), &smem);
+  k<<<grid, 256, smem, st>>>(t, n, tt, codes, absmax, flag, fo);
+  return check_cuda(cudaGetLastError(), "drq_tma_kernel launch");
+}
+
+template <int IB, int OB, typename FO>
+static int drq_tma_ns(const SrcTable& t, int n_src, int64_t n, int64_t in_block, uint8_t* codes, double* absmax,
+                      FO* fo, uint32_t* flag, cudaStream_t st) {
+  switch (n_src) {
+    case 2: return run_drq_tma<IB, OB, 2, FO>(t, n, in_block, codes, absmax, fo, flag, st);
+    case 4: return run_drq_tma<IB, OB, 4, FO>(t, n, in_block, codes, absmax, fo, flag, st);
+    case 8: return run_drq_tma<IB, OB, 8, FO>(t, n, in_block, codes, absmax, fo, flag, st);
+  }
+  return fail(ZPP_ERR_VALIDATION, "no TMA K2 for this fan-in");
+}
+
+template <typename FO>
+static int drq_tma_bits(const SrcTable& t, int n_src, int64_t n, int in_bits, int64_t in_block, int out_bits,
+                        uint8_t* codes, double* absmax, FO* fo, uint32_t* flag, cudaStream_t st) {
+  if (in_bits == 4 && out_bits == 4) return drq_tma_ns<4, 4, FO>(t, n_src, n, in_block, codes, absmax, fo, flag, st);
+  if (in_bits == 8 && out_bits == 4) return drq_tma_ns<8, 4, FO>(t, n_src, n, in_block, codes, absmax, fo, flag, st);
+  if (in_bits == 4 && out_bits == 8) return drq_tma_ns<4, 8, FO>(t, n_src, n, in_block, codes, absmax, fo, flag, st);
+  return drq_tma_ns<8, 8, FO>(t, n_src, n, in_block, codes, absmax, fo, flag, st);
+}
+
+int launch_drq_tma(const void* const* codes, const void* const* absmax, int n_src, int64_t n, int in_bits,
+                   int64_t in_block, int out_bits, int64_t out_block, uint8_t* out_codes, double* out_absmax,
+                   void* final_out, int final_dtype, uint32_t* flag, cudaStream_t st, bool* handled) {
+  *handled = false;
+  if (n <= 0 || n % 16 || out_block != 512 || in_block % 16 || (in_block & (in_block - 1)) ||
+      !(n_src == 2 || n_src == 4 || n_src == 8))
+    return ZPP_OK;
+  if (final_out && final_dtype != ZPP_F32 && final_dtype != ZPP_F64) return ZPP_OK;
+  SrcTable t;
+  int rc = fill_table(t, codes, absmax, n_src);
+  if (rc) return rc;
+  for (int i = 0; i < n_src; ++i)
+    if (reinterpret_cast<uintptr_t>(codes[i]) % 16) return ZPP_OK;
+  *handled = true;
+  if (!final_out)
+    return drq_tma_bits<void>(t, n_src, n, in_bits, in_block, out_bits, out_codes, out_absmax, nullptr, flag, st);
+  if (final_dtype == ZPP_F32)
+    return drq_tma_bits<float>(t, n_src, n, in_bits, in_block, out_bits, nullptr, out_absmax,
+                               reinterpret_cast<float*>(final_out), flag, st);
+  return drq_tma_bits<double>(t, n_src, n, in_bits, in_block, out_bits, nullptr, out_absmax,
+                              reinterpret_cast<double*>(final_out), flag, st);
+}
+
+template <int B, int NS, typename O>
+static int run_dr_tma(const SrcTable& t, int64_t n, int64_t block, O* out, uint32_t* flag, cudaStream_t st) {
+  const TmaTile tt = tma_tile(NS, B, block, sizeof(double));
+  auto k = dr_tma_kernel<B, NS, O, kTmaStages>;
+  size_t smem = 0;
+  const int grid = tma_grid(k, tt, ceil_div(n / 16, tt.tu), &smem);
+  k<<<grid, 256, smem, st>>>(t, n, tt, out, flag);
+  return check_cuda(cudaGetLastError(), "dr_tma_kernel launch");
+}
+
+template <int B, typename O>
+static int dr_tma_ns(const SrcTable& t, int n_src, int64_t n, int64_t block, O* out, uint32_t* flag,
+                     cudaStream_t st) {
+  switch (n_src) {
+    case 2: return run_dr_tma<B, 2, O>(t, n, block, out, flag, st);
+    case 4: return run_dr_tma<B, 4, O>(t, n, block, out, flag, st);
+    case 8: return run_dr_tma<B, 8, O>(t, n, block, out, flag, st);
+  }
+  return fail(ZPP_ERR_VALIDATION, "no TMA K3 for this fan-in");
+}
+
+int launch_dr_tma(const void* const* codes, const void* const* absmax_f64, int n_src, int64_t n, int bits,
+                  int64_t block, void* out, int out_dtype, uint32_t* flag, cudaStream_t st, bool* handled) {
+  *handled = false;
+  if (n <= 0 || n % 16 || block % 16 || (block & (block - 1)) || !(n_src == 2 || n_src == 4 || n_src == 8) ||
+      (out_dtype != ZPP_F32 && out_dtype != ZPP_F64) || !aligned16(out))
+    return ZPP_OK;
+  SrcTable t;
+  int rc = fill_table(t, codes, absmax_f64, n_src);
+  if (rc) return rc;
+  for (int i = 0; i < n_src; ++i)
+    if (reinterpret_cast<uintptr_t>(codes[i]) % 16) return ZPP_OK;
+  *handled = true;
+  if (out_dtype == ZPP_F32)
+    return bits == 8 ? dr_tma_ns<8, float>(t, n_src, n, block, reinterpret_cast<float*>(out), flag, st)
+                     : dr_tma_ns<4, float>(t, n_src, n, block, reinterpret_cast<float*>(out), flag, st);
+  return bits == 8 ? dr_tma_ns<8, double>(t, n_src, n, block, reinterpret_cast<double*>(out), flag, st)
+                   : dr_tma_ns<4, double>(t, n_src, n, block, reinterpret_cast<double*>(out), flag, st);
 }
 
 }  // namespace zpp

@@ -263,6 +263,23 @@ class Communicator:
                    "qgz_reduce_scatter")
         return out
 
+    TRACE_STAGES = ("begin", "quantize", "barrier", "gather", "K1", "K2", "K3")
+
+    def trace(self, enable: bool = True) -> None:
+        """Record timing events between the launches of each qwZ / qgZ call
+        (diagnostics; read them with trace_read)."""
+        _lib.check(self.lib.zpp_comm_trace(self.handle, 1 if enable else 0), "zpp_comm_trace")
+
+    def trace_read(self) -> list[tuple[str, float]]:
+        """[(stage just finished, ms since the last traced call began)]; waits
+        for that call to finish."""
+        ids = (ctypes.c_int * 32)()
+        ms = (ctypes.c_float * 32)()
+        n = self.lib.zpp_comm_trace_read(self.handle, ids, ms, 32)
+        if n < 0:
+            _lib.check(-n, "zpp_comm_trace_read")
+        return [(self.TRACE_STAGES[ids[i]], float(ms[i])) for i in range(n)]
+
     def barrier(self, scope: str = "world", timeout_ms: int = 60000):
         code = {"world": 0, "group": 1, "cross": 2}[scope]
         _lib.check(self.lib.zpp_comm_barrier(self.handle, code, timeout_ms, self.flag.data_ptr(), stream_ptr()),

@@ -343,7 +343,7 @@ def test_exact_ties_bf16(bits):
     assert np.array_equal(q.scales.cpu().numpy(), s)
 
 
-@pytest.mark.parametrize("n_src", [1, 3, 5, 8])
+@pytest.mark.parametrize("n_src", [1, 2, 3, 4, 5, 8])
 @pytest.mark.parametrize("bits,block,n", [(4, 512, 8192 + 512), (8, 2048, 3 * 2048 + 16), (8, 40, 999),
                                           (4, 24, 1000)])
 def test_dequant_reduce_many_sources(n_src, bits, block, n):

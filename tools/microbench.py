@@ -77,10 +77,18 @@ def main():
         torch.cuda.empty_cache()
     if only == "codec":
         return
-    # qgZ kernels at the W=8 bucket shape, emulated on one GPU (X=4, Y=2)
+    # qgZ kernels at the bucket shapes of W=8 (X=4, Y=2) and W=4 (2x2), emulated
+    # on one GPU (all sources local)
+    for X, Y in ((4, 2), (2, 2)):
+        qgz_shape(lib, st, flag, X, Y)
+    torch.cuda.synchronize()
+    print("flag", int(flag.item()))
+
+
+def qgz_shape(lib, st, flag, X, Y):
     n = 134_217_728
     g = (torch.randn(n, device="cuda") * 1e-3).bfloat16()
-    X, Y, S = 4, 2, 1
+    S = 1
     L = n // (S * X * Y)
     send = zpp.quantizer.alloc_quantized(X * Y * L, zpp.QuantConfig(bit_width=4, block_size=512))
 
@@ -110,8 +118,6 @@ def main():
         lib.zpp_dequant_reduce(cp3, ap3, _lib.F64, Y, L, 4, 512, res.data_ptr(), _lib.F32, 1.0, flag.data_ptr(), st)
     t = timeit(k3)
     report(f"K3 dequant-reduce Y={Y} n={L}", t, Y * (L // 2 + L // 512 * 8) + L * 4)
-    torch.cuda.synchronize()
-    print("flag", int(flag.item()))
 
 
 if __name__ == "__main__":
