@@ -78,3 +78,27 @@ def test_world1_fused_round_trip(dtype, bits, block):
     got = out.to(torch.float64).cpu().numpy()
     assert np.array_equal(got, gu.round_to(want, dtype))
     comm.close()
+
+
+def test_stage_tracer():
+    """zpp_comm_trace: one event per launched stage of the last qgZ / qwZ
+    call, in launch order, with non-decreasing times (diagnostics used by
+    tools/stage_timeline.py)."""
+    import paper_2306_10209_b200 as zpp
+    from paper_2306_10209_b200.dist import Communicator
+
+    comm = Communicator(qwz_shard=4096, qgz_elems=8192, qgz_stages=2,
+                        qgz_cfg=zpp.QuantConfig(bit_width=4, block_size=512))
+    g = torch.randn(8192, device="cuda").bfloat16()
+    comm.qgz_reduce_scatter(g)
+    assert comm.trace_read() == []  # tracing off: nothing recorded
+    comm.trace(True)
+    comm.qgz_reduce_scatter(g)
+    tr = comm.trace_read()
+    assert [s for s, _ in tr] == ["begin", "K1", "barrier", "K2", "K1", "barrier", "K2"]
+    assert all(b >= a for (_, a), (_, b) in zip(tr, tr[1:]))
+    comm.qwz_allgather(torch.randn(4096, device="cuda").half())
+    assert [s for s, _ in comm.trace_read()] == ["begin"]  # world of 1: one fused launch
+    comm.trace(False)
+    comm.check()
+    comm.close()
