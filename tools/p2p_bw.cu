@@ -146,5 +146,49 @@ int main() {
       printf("%d GPUs  %-44s grid %4d: %.3f ms  ingress %.0f GB/s per GPU\n", ng, names[mode], G, worst, gbs);
     }
   }
+  // copy engines: one cudaMemcpyAsync per peer on its own stream (pull: the
+  // receiving device's streams read the peer; push: the sender's streams write)
+  std::vector<std::vector<cudaStream_t>> ps(ng, std::vector<cudaStream_t>(ng));
+  for (int d = 0; d < ng; ++d) {
+    CK(cudaSetDevice(d));
+    for (int e = 0; e < ng; ++e) CK(cudaStreamCreateWithFlags(&ps[d][e], cudaStreamNonBlocking));
+  }
+  for (int push = 0; push < 2; ++push) {
+    float worst = 0;
+    for (int rep = 0; rep < 4; ++rep) {
+      std::vector<cudaEvent_t> a(ng), b(ng);
+      for (int d = 0; d < ng; ++d) { CK(cudaSetDevice(d)); CK(cudaDeviceSynchronize()); }
+      for (int d = 0; d < ng; ++d) {
+        CK(cudaSetDevice(d));
+        CK(cudaEventCreate(&a[d]));
+        CK(cudaEventCreate(&b[d]));
+        CK(cudaEventRecord(a[d], st[d]));
+        for (int e = 0; e < ng; ++e) {
+          if (e == d) continue;
+          CK(cudaStreamWaitEvent(ps[d][e], a[d], 0));
+          if (!push) CK(cudaMemcpyAsync(recv[d] + S * e, send[e] + S * d, S, cudaMemcpyDeviceToDevice, ps[d][e]));
+          else CK(cudaMemcpyAsync(recv[e] + S * d, send[d] + S * e, S, cudaMemcpyDeviceToDevice, ps[d][e]));
+          cudaEvent_t j;
+          CK(cudaEventCreateWithFlags(&j, cudaEventDisableTiming));
+          CK(cudaEventRecord(j, ps[d][e]));
+          CK(cudaStreamWaitEvent(st[d], j, 0));
+        }
+        CK(cudaEventRecord(b[d], st[d]));
+      }
+      float mx = 0;
+      for (int d = 0; d < ng; ++d) {
+        CK(cudaSetDevice(d));
+        CK(cudaEventSynchronize(b[d]));
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, a[d], b[d]));
+        mx = ms > mx ? ms : mx;
+      }
+      if (rep > 0) worst = mx > worst ? mx : worst;
+    }
+    const double gbs = (double)S * (ng - 1) / (worst * 1e-3) / 1e9;
+    printf("%d GPUs  %-44s          : %.3f ms  ingress %.0f GB/s per GPU\n", ng,
+           push ? "push_ce (cudaMemcpyAsync per peer, sender)" : "pull_ce (cudaMemcpyAsync per peer, receiver)", worst,
+           gbs);
+  }
   return 0;
 }
