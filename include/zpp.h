@@ -111,6 +111,19 @@ int zpp_dequant_reduce_quant(const void* const* codes, const void* const* absmax
                              void* errflag, void* stream);
 size_t zpp_drq_workspace_bytes(int64_t n, int64_t out_block);
 
+/* QuantizedTensor.to_bytes on the device (replaces zs/quantizer.py:121-131):
+ * writes the canonical wire layout -- 13-byte '<QBI' header (original_len,
+ * bit_width, block_size), ceil(n/block) fp16 scales (RN-even of the f64 scale),
+ * then the packed codes incl. padding -- into `out` (device, unaligned ok;
+ * 13 + 2*n_blocks + code bytes long). */
+int zpp_wire_pack(const void* codes, const void* absmax, int absmax_dtype, int64_t n, int bits, int64_t block,
+                  void* out, void* stream);
+/* QuantizedTensor.from_bytes payload on the device (zs/quantizer.py:133-149):
+ * `raw` is the whole wire buffer (header already validated by the host);
+ * writes the codes and an f64 absmax = fp16 scale * qmax (exact). */
+int zpp_wire_unpack(const void* raw, int64_t n, int bits, int64_t block, void* codes, void* absmax_f64,
+                    void* stream);
+
 /* QuantizedTensor.scales: f64(absmax)/qmax, bit-exact (zs/quantizer.py:219) */
 int zpp_scales(const void* absmax, int absmax_dtype, int64_t n_blocks, int bits, void* out_f64, void* stream);
 

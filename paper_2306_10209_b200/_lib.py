@@ -43,6 +43,8 @@ SIGNATURES = {
                                          P, P, P, c_size_t, P, P]),
     "zpp_drq_workspace_bytes": (c_size_t, [c_int64, c_int64]),
     "zpp_scales": (c_int, [P, c_int, c_int64, c_int, P, P]),
+    "zpp_wire_pack": (c_int, [P, P, c_int, c_int64, c_int, c_int64, P, P]),
+    "zpp_wire_unpack": (c_int, [P, c_int64, c_int, c_int64, P, P, P]),
     "zpp_comm_create": (c_int, [c_int, c_int, c_int, c_size_t, ctypes.POINTER(c_void_p)]),
     "zpp_comm_ipc_handle": (c_int, [P, P]),
     "zpp_comm_open_peers": (c_int, [P, P]),

@@ -1,4 +1,5 @@
 // Host launchers + C ABI for the codec kernels (K0..K4).
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -376,6 +377,55 @@ int zpp_scales(const void* absmax, int absmax_dtype, int64_t n_blocks, int bits,
     return fail(ZPP_ERR_VALIDATION, "absmax dtype must be F32 or F64");
   }
   return check_cuda(cudaGetLastError(), "scales_kernel launch");
+}
+
+int zpp_wire_pack(const void* codes, const void* absmax, int absmax_dtype, int64_t n, int bits, int64_t block,
+                  void* out, void* stream) {
+  int rc = check_cfg(bits, block);
+  if (rc) return rc;
+  if (n < 0 || (n > 0 && (!codes || !absmax)) || !out) return fail(ZPP_ERR_VALIDATION, "bad arguments");
+  if (absmax_dtype != ZPP_F32 && absmax_dtype != ZPP_F64)
+    return fail(ZPP_ERR_VALIDATION, "absmax dtype must be F32 or F64");
+  const int64_t nb = ceil_div(n, block);
+  const int64_t cb = code_bytes(n, bits, block);
+  // '<QBI': u64 original_len, u8 bit_width, u32 block_size, little endian
+  const uint64_t lo = (uint64_t)n;
+  const uint64_t hi = (uint64_t)(uint8_t)bits | ((uint64_t)(uint32_t)block << 8);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(nb + 13, 256), 8 * sm_count()));
+  uint8_t* o = reinterpret_cast<uint8_t*>(out);
+  if (absmax_dtype == ZPP_F32) {
+    auto a = reinterpret_cast<const float*>(absmax);
+    if (bits == 8) wire_pack_kernel<8, float><<<grid, 256, 0, st>>>(a, nb, lo, hi, o);
+    else wire_pack_kernel<4, float><<<grid, 256, 0, st>>>(a, nb, lo, hi, o);
+  } else {
+    auto a = reinterpret_cast<const double*>(absmax);
+    if (bits == 8) wire_pack_kernel<8, double><<<grid, 256, 0, st>>>(a, nb, lo, hi, o);
+    else wire_pack_kernel<4, double><<<grid, 256, 0, st>>>(a, nb, lo, hi, o);
+  }
+  rc = check_cuda(cudaGetLastError(), "wire_pack_kernel launch");
+  if (rc || cb == 0) return rc;
+  return check_cuda(cudaMemcpyAsync(o + 13 + 2 * nb, codes, (size_t)cb, cudaMemcpyDeviceToDevice, st),
+                    "wire codes copy");
+}
+
+int zpp_wire_unpack(const void* raw, int64_t n, int bits, int64_t block, void* codes, void* absmax_f64, void* stream) {
+  int rc = check_cfg(bits, block);
+  if (rc) return rc;
+  if (n < 0 || !raw || (n > 0 && (!codes || !absmax_f64))) return fail(ZPP_ERR_VALIDATION, "bad arguments");
+  const int64_t nb = ceil_div(n, block);
+  const int64_t cb = code_bytes(n, bits, block);
+  if (nb == 0) return ZPP_OK;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(nb, 256), 8 * sm_count()));
+  auto r = reinterpret_cast<const uint8_t*>(raw);
+  auto a = reinterpret_cast<double*>(absmax_f64);
+  if (bits == 8) wire_unpack_kernel<8><<<grid, 256, 0, st>>>(r, nb, a);
+  else wire_unpack_kernel<4><<<grid, 256, 0, st>>>(r, nb, a);
+  rc = check_cuda(cudaGetLastError(), "wire_unpack_kernel launch");
+  if (rc) return rc;
+  return check_cuda(cudaMemcpyAsync(codes, r + 13 + 2 * nb, (size_t)cb, cudaMemcpyDeviceToDevice, st),
+                    "wire codes copy");
 }
 
 }  // extern "C"

@@ -1860,6 +1860,69 @@ dr_tma_kernel(SrcTable src, int64_t n, TmaTile tt, O* __restrict__ out, uint32_t
   if (bad) raise_flag(flag, FLAG_BADCODE);
 }
 
+// Wire format on the device (QuantizedTensor.to_bytes / from_bytes,
+// zs/quantizer.py:121-149): 13-byte '<QBI' header, fp16 scales, packed codes
+// (incl. padding), contiguous and unaligned after the header.
+
+// f64 -> fp16 bits, round to nearest even, subnormals and overflow to inf
+// included (numpy's float64.astype(float16), zs/quantizer.py:130), in integer
+// arithmetic so no intermediate rounding can intervene.
+__device__ __forceinline__ uint16_t f64_to_f16_bits(double x) {
+  const uint64_t b = (uint64_t)__double_as_longlong(x);
+  const uint16_t sign = (uint16_t)((b >> 48) & 0x8000u);
+  const int e = (int)((b >> 52) & 0x7FF);
+  const uint64_t man = b & ((1ull << 52) - 1);
+  if (e == 0x7FF) return sign | (man ? 0x7E00u : 0x7C00u);
+  const int ue = e - 1023;        // unbiased exponent
+  if (ue < -25) return sign;      // below half the smallest subnormal (2^-25 ties to even: 0)
+  const uint64_t sig = (1ull << 52) | man;  // e > 0 here (f64 subnormals are < 2^-25)
+  // fp16 value = sig * 2^(ue-52); in units of 2^-24 (subnormal ulp) when
+  // ue < -14, else with an implicit bit and a 10-bit mantissa
+  const int shift = ue < -14 ? (52 - (ue + 24)) : 42;
+  uint64_t m = sig >> shift;
+  const uint64_t rem = sig & ((1ull << shift) - 1), half = 1ull << (shift - 1);
+  if (rem > half || (rem == half && (m & 1))) ++m;
+  if (ue < -14) return sign | (uint16_t)m;  // m <= 1024: 1024 is the smallest normal, 0x0400
+  int E = ue + 15;
+  if (m == (1ull << 11)) {  // mantissa overflowed into the next binade
+    m >>= 1;
+    ++E;
+  }
+  if (E >= 31) return sign | 0x7C00u;
+  return sign | (uint16_t)(E << 10) | (uint16_t)(m & 0x3FF);
+}
+
+__device__ __forceinline__ void st_u8(uint8_t* p, uint32_t v) {
+  asm volatile("st.global.u8 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// pack: header + fp16 scales (the codes follow by a device-to-device copy)
+template <int BITS, typename A>
+__global__ void wire_pack_kernel(const A* __restrict__ absmax, int64_t nb, uint64_t hdr_lo, uint64_t hdr_hi,
+                                 uint8_t* __restrict__ out) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i0 < 13) st_u8(out + i0, (uint32_t)((i0 < 8 ? (hdr_lo >> (8 * i0)) : (hdr_hi >> (8 * (i0 - 8)))) & 0xFF));
+  for (int64_t b = i0; b < nb; b += stride) {
+    const uint32_t u = f64_to_f16_bits(scale_of<BITS>(absmax_f64<A>(absmax, b)));
+    st_u8(out + 13 + 2 * b, u & 0xFF);
+    st_u8(out + 14 + 2 * b, u >> 8);
+  }
+}
+
+// unpack: fp16 wire scales -> f64 absmax = scale16 * qmax (exact), codes copied
+// (the codes are copied device-to-device by the host)
+template <int BITS>
+__global__ void wire_unpack_kernel(const uint8_t* __restrict__ raw, int64_t nb, double* __restrict__ absmax) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (int64_t b = i0; b < nb; b += stride) {
+    const uint32_t lo = raw[13 + 2 * b], hi = raw[14 + 2 * b];
+    const uint16_t u = (uint16_t)(lo | (hi << 8));
+    absmax[b] = __dmul_rn((double)__half2float(__ushort_as_half(u)), (double)Codes<BITS>::kQmax);
+  }
+}
+
 // f64 scales from absmax (QuantizedTensor.scales; zs/quantizer.py:219)
 template <int BITS, typename A>
 __global__ void scales_kernel(const A* __restrict__ absmax, int64_t nb, double* __restrict__ out) {

@@ -175,11 +175,20 @@ class QuantizedTensor:
                                               self.config.bit_width, out.data_ptr(), stream_ptr()), "scales")
         return out
 
+    def to_wire(self) -> torch.Tensor:
+        """Canonical wire layout (zs/quantizer.py:121-131) built on the device:
+        a uint8 device tensor [header | fp16 scales | codes] (zpp_wire_pack)."""
+        n_bytes = _HEADER.size + self.n_blocks * SCALE_WIRE_BYTES + int(self.codes.numel())
+        out = torch.empty(n_bytes, dtype=torch.uint8, device=self.codes.device)
+        _lib.check(_lib.load().zpp_wire_pack(self.codes.data_ptr(), self.absmax.data_ptr(), self.absmax_code,
+                                             self.original_len, self.config.bit_width, self.config.block_size,
+                                             out.data_ptr(), stream_ptr()), "to_bytes")
+        return out
+
     def to_bytes(self) -> bytes:
-        """Canonical wire layout (zs/quantizer.py:121-131): header, fp16 scales, codes."""
-        header = _HEADER.pack(self.original_len, self.config.bit_width, self.config.block_size)
-        scales16 = self.scales.cpu().numpy().astype(np.float16).tobytes()
-        return header + scales16 + self.codes.cpu().numpy().tobytes()
+        """Canonical wire layout (zs/quantizer.py:121-131): header, fp16 scales,
+        codes -- packed on the device, one device-to-host copy."""
+        return self.to_wire().cpu().numpy().tobytes()
 
     @classmethod
     def from_bytes(cls, raw: bytes) -> "QuantizedTensor":
@@ -189,12 +198,13 @@ class QuantizedTensor:
         ``scale16 * qmax`` (exact in f64), from which every kernel recovers
         ``scale16`` bit-exactly (``RN64(scale16*qmax/qmax) == scale16``)."""
         original_len, cfg, n_blocks, scale_end = from_bytes_header(raw)
-        scales16 = np.frombuffer(raw, dtype=np.float16, count=n_blocks, offset=_HEADER.size)
-        absmax = scales16.astype(np.float64) * cfg.qmax
-        codes = np.frombuffer(raw, dtype=np.uint8, offset=scale_end).copy()
         dev = device()
-        return cls(codes=torch.from_numpy(codes).to(dev), absmax=torch.from_numpy(absmax).to(dev),
-                   original_len=original_len, config=cfg)
+        wire = torch.frombuffer(bytearray(raw), dtype=torch.uint8).to(dev)  # one host-to-device copy
+        codes = torch.empty(len(raw) - scale_end, dtype=torch.uint8, device=dev)
+        absmax = torch.empty(n_blocks, dtype=torch.float64, device=dev)
+        _lib.check(_lib.load().zpp_wire_unpack(wire.data_ptr(), original_len, cfg.bit_width, cfg.block_size,
+                                               codes.data_ptr(), absmax.data_ptr(), stream_ptr()), "from_bytes")
+        return cls(codes=codes, absmax=absmax, original_len=original_len, config=cfg)
 
     def slice_blocks(self, start: int, length: int) -> "QuantizedTensor":
         """Elements [start, start+length) as a zero-copy view (zs/quantizer.py:151-169)."""

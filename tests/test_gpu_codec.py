@@ -398,3 +398,29 @@ def test_fused_fixed_fanin_fast_path(n_src):
     qs[-1].codes[100] = 0x88  # two -8 nibbles
     with pytest.raises(zpp.IntegrityError):
         zpp.fused_dequant_reduce_quant(qs, zpp.QuantConfig(bit_width=4, block_size=512))
+
+
+@pytest.mark.parametrize("bits,block", [(8, 64), (4, 32), (8, 2048)])
+def test_to_bytes_device_pack_matches_reference_layout(bits, block):
+    """zpp_wire_pack (to_bytes on the device) == the reference's layout built
+    on the host: '<QBI' header, numpy float16 of the f64 scales (RN-even,
+    fp16 subnormals and overflow to inf included), codes with padding
+    (zs/quantizer.py:121-131); from_bytes on the device inverts it."""
+    import struct
+
+    zpp = _zpp()
+    rng = np.random.default_rng(bits * 1000 + block)
+    n = 40 * block + block // 2 + 8
+    mags = 10.0 ** rng.uniform(-9, 7, size=(n + block - 1) // block)  # scales spanning fp16's range
+    x = rng.normal(size=n) * np.repeat(mags, block)[:n]
+    q = zpp.quantize(torch.from_numpy(x).cuda(), zpp.QuantConfig(bit_width=bits, block_size=block))
+    c, s, _ = O.quantize(x, bits, block)
+    with np.errstate(over="ignore"):
+        want = struct.pack("<QBI", n, bits, block) + s.astype(np.float16).tobytes() + c.tobytes()
+    got = q.to_bytes()
+    assert got == want
+    back = zpp.QuantizedTensor.from_bytes(got)
+    assert np.array_equal(back.codes.cpu().numpy(), c)
+    with np.errstate(over="ignore"):
+        want_abs = s.astype(np.float16).astype(np.float64) * (2 ** (bits - 1) - 1)
+    assert np.array_equal(back.absmax.cpu().numpy(), want_abs)
