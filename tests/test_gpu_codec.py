@@ -424,3 +424,18 @@ def test_to_bytes_device_pack_matches_reference_layout(bits, block):
     with np.errstate(over="ignore"):
         want_abs = s.astype(np.float16).astype(np.float64) * (2 ** (bits - 1) - 1)
     assert np.array_equal(back.absmax.cpu().numpy(), want_abs)
+
+
+def test_tma_fed_reduce_kernels_on_one_gpu():
+    """The TMA-fed K2 / K3 (drq_tma_kernel, dr_tma_kernel) normally run only in
+    multi-GPU qgZ; ZPP_FORCE_TMA=1 routes the public entry points to them so
+    the fused and reduce parity tests above cover them on a single GPU too."""
+    import os
+    import subprocess
+    import sys
+
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider", os.path.abspath(__file__),
+                        "-k", "fused_fixed_fanin or dequant_reduce_many_sources"],
+                       env={**os.environ, "ZPP_FORCE_TMA": "1"}, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout
