@@ -386,6 +386,10 @@ def run_ours(args):
     extra["zeropp_step_13b_layer"] = step_leg(world=world, dev=dev, g=g, timed=lambda f: timed(f, max(5, args.steps // 2), 2),
                                               oversub=oversub, comm_cls=Communicator, zpp=zpp,
                                               nccl_allgather=nccl_allgather, nccl_reduce_scatter=nccl_reduce_scatter)
+    kq_gbs = kern["quantize_reg_kernel"]["GBps"]
+    extra["quant_kernel_hbm"] = {"kernel": "quantize_reg_kernel (K0: fp16 shard -> INT8/2048 codes + absmax)",
+                                 "achieved_GBps": kq_gbs, "frac_of_8TBs_nominal": kq_gbs / 8000.0,
+                                 "frac_of_measured_peak": kq_gbs / hbm_peak, "shard_elems": shard_len}
     extra["params_per_s"] = {"qwz": world * M_PARAMS / t_step, "qgz": world * QGZ_BUCKET / t_qgz,
                              "note": "whole-job parameters (or gradients) delivered per second"}
     if world > 1:
