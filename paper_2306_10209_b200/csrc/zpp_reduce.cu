@@ -257,8 +257,14 @@ static constexpr int kTmaStages = 3;
 static TmaTile tma_tile(int n_src, int bits, int64_t block, size_t abs_size) {
   TmaTile tt;
   const int ub = 2 * bits;
+  // code bytes of all sources per ring stage: 12 KB measured best on 4 B200s
+  // (qgZ 1x4 K2 97 us vs 103-110 at 24 KB and 124 at 48 KB; 2x2 K3 54 vs 64 us)
+  static const int64_t budget = [] {
+    const char* e = getenv("ZPP_TMA_STAGE_BYTES");
+    return (int64_t)(e ? atoi(e) : 12288);
+  }();
   int tu = 4096;
-  while (tu > 32 && (int64_t)n_src * tu * ub > 24576) tu >>= 1;
+  while (tu > 32 && (int64_t)n_src * tu * ub > budget) tu >>= 1;
   tt.tu = tu;
   tt.lg = __builtin_ctzll((unsigned long long)block);
   tt.code_slot = (int)((tu * ub + 15) & ~15);
