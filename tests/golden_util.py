@@ -55,7 +55,7 @@ def f64_to_bf16_rne(x: np.ndarray) -> np.ndarray:
     x = np.asarray(x, dtype=np.float64)
     m, e = np.frexp(x)
     q = np.ldexp(1.0, np.maximum(e - 8, -133))
-    with np.errstate(over="ignore"):
+    with np.errstate(over="ignore", invalid="ignore"):  # sign(0) * inf; zeros are restored below
         r = np.rint(x / q) * q
         r = np.where(np.abs(r) > 3.3895313892515355e38, np.sign(x) * np.inf, r)
     return np.where(x == 0, x, r)
