@@ -146,6 +146,15 @@ size_t zpp_comm_sym_bytes(zpp_comm_t comm);
 /* device barrier among ranks: scope 0 = world, 1 = my group, 2 = my cross set
  * (same local index in every group).  Bounded spin (timeout_ms). */
 int zpp_comm_barrier(zpp_comm_t comm, int scope, int timeout_ms, void* errflag, void* stream);
+/* After a barrier TIMEOUT (errflag bit 4) every data kernel sharing that flag
+ * returns without touching its buffers.  Recovery: every rank synchronises
+ * its device and passes a host barrier, then calls zpp_comm_reset (zeroes this
+ * rank's barrier flag words, restarts the epochs and double-buffer phases),
+ * clears errflag, and passes a second host barrier.  No reference
+ * counterpart: the simulated fabric (zs/simnet.py) cannot time out. */
+int zpp_comm_reset(zpp_comm_t comm);
+/* Frees this rank's symmetric buffer.  Peers may still read it: call only
+ * after every rank has synchronised and passed a host barrier. */
 int zpp_comm_destroy(zpp_comm_t comm);
 /* Stage tracer (diagnostics; not in the reference): while enabled, each qwZ /
  * qgZ call records timing events on its stream after every launch.

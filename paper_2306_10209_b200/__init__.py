@@ -62,7 +62,6 @@ from .collectives import (
     reorder_mapping,
 )
 from .accounting import BWD_GATHER, FWD_GATHER, GRAD_REDUCE, StepConfig, step_volumes
-from .engine import StepRecord, ToyTaskConfig, TrainingEngine, TrainRecord, ZeroConfig, train_toy
 
 __version__ = "0.1.0"
 
@@ -78,6 +77,5 @@ __all__ = [
     "ReorderPermutation", "all_gather_baseline", "all_gather_qwz", "reduce_scatter_ring", "reorder_mapping",
     "qgz_2hop", "qgz_1hop", "reduce_scatter_ring_naive_quant",
     "StepConfig", "step_volumes", "FWD_GATHER", "BWD_GATHER", "GRAD_REDUCE",
-    "ToyTaskConfig", "ZeroConfig", "TrainingEngine", "TrainRecord", "StepRecord", "train_toy",
     "__version__",
 ]

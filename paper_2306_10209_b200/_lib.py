@@ -51,6 +51,7 @@ SIGNATURES = {
     "zpp_comm_sym_ptr": (c_void_p, [P, c_int]),
     "zpp_comm_sym_bytes": (c_size_t, [P]),
     "zpp_comm_barrier": (c_int, [P, c_int, c_int, P, P]),
+    "zpp_comm_reset": (c_int, [P]),
     "zpp_comm_destroy": (c_int, [P]),
     "zpp_comm_trace": (c_int, [P, c_int]),
     "zpp_comm_trace_read": (c_int, [P, P, P, c_int]),

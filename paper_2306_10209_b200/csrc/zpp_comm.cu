@@ -36,6 +36,7 @@ struct BarrierArgs {
 };
 
 __global__ void barrier_kernel(BarrierArgs a, int n, uint32_t epoch, uint64_t timeout_ns, uint32_t* flag) {
+  if (comm_aborted(flag)) return;  // an earlier barrier timed out: stay stopped until the host resets
   const int t = threadIdx.x;
   __threadfence_system();
   __syncthreads();
@@ -61,7 +62,9 @@ __global__ void barrier_kernel(BarrierArgs a, int n, uint32_t epoch, uint64_t ti
 
 // byte copy of n_src peer segments into out (hpZ gather), 16 B vectors when aligned
 __global__ void __launch_bounds__(256)
-gather_copy_kernel(SrcTable src, int n_src, int rot, int64_t seg_bytes, uint8_t* __restrict__ out, int vec) {
+gather_copy_kernel(SrcTable src, int n_src, int rot, int64_t seg_bytes, uint8_t* __restrict__ out, int vec,
+                   const uint32_t* flag) {
+  if (comm_aborted(flag)) return;
   const int lane = threadIdx.x & 31;
   const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarp = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -93,7 +96,9 @@ constexpr int kCopyStages = 4;
 constexpr int kCopyTile = 8192;  // bytes
 
 __global__ void __launch_bounds__(256)
-gather_copy_tma_kernel(SrcTable src, int n_src, int rot, int64_t seg_bytes, uint8_t* __restrict__ out) {
+gather_copy_tma_kernel(SrcTable src, int n_src, int rot, int64_t seg_bytes, uint8_t* __restrict__ out,
+                       const uint32_t* flag) {
+  if (comm_aborted(flag)) return;
   extern __shared__ __align__(128) uint8_t dsm[];
   uint8_t* ring = dsm;
   uint64_t* full = reinterpret_cast<uint64_t*>(dsm + kCopyStages * kCopyTile);
@@ -151,6 +156,7 @@ struct zpp_comm {
   bool opened[kMaxRanks] = {};
   uint32_t epoch[kScopes] = {};
   uint64_t qwz_uses = 0, qgz_uses = 0;
+  size_t qwz_region = 0;  // region size of the last qwZ call
   size_t qgz_region = 0;  // region size of the last qgZ call
   cudaIpcMemHandle_t handle;
   int device = 0;
@@ -284,6 +290,21 @@ int zpp_comm_barrier(zpp_comm_t c, int scope, int timeout_ms, void* errflag, voi
   return barrier(c, scope, timeout_ms, reinterpret_cast<uint32_t*>(errflag), reinterpret_cast<cudaStream_t>(stream));
 }
 
+int zpp_comm_reset(zpp_comm_t c) {
+  if (!c) return fail(ZPP_ERR_VALIDATION, "null communicator");
+  // The caller has synchronised every rank's device and passed a host barrier
+  // (Communicator.recover), so no barrier kernel or peer read is in flight:
+  // zero this rank's flag words and restart every epoch and double-buffer
+  // phase from the state zpp_comm_create leaves.
+  int rc = check_cuda(cudaDeviceSynchronize(), "reset sync");
+  if (!rc) rc = check_cuda(cudaMemset(c->local + c->sym_bytes, 0, kFlagBytes), "flag memset");
+  if (rc) return rc;
+  for (int s = 0; s < kScopes; ++s) c->epoch[s] = 0;
+  c->qwz_uses = c->qgz_uses = 0;
+  c->qwz_region = c->qgz_region = 0;
+  return check_cuda(cudaDeviceSynchronize(), "reset sync");
+}
+
 int zpp_comm_destroy(zpp_comm_t c) {
   if (!c) return ZPP_OK;
   cudaDeviceSynchronize();
@@ -331,6 +352,15 @@ int zpp_qwz_allgather(zpp_comm_t c, size_t sym_offset, const void* shard, int dt
   trace_mark(c, TR_BEGIN, reinterpret_cast<cudaStream_t>(stream));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   uint32_t* flag = reinterpret_cast<uint32_t*>(errflag);
+  // A different shard length moves the half boundaries, so K0 of this call
+  // could overwrite codes peers are still pulling for the previous call (a
+  // rank passing that call's barrier only proves peers finished its K0, not
+  // its gather).  Drain every rank's reads of the old layout first -- the same
+  // guard qgZ takes below.
+  if (c->world > 1 && c->qwz_region != 0 && c->qwz_region != region) {
+    if ((rc = barrier(c, 0, kBarrierTimeoutMs, flag, st))) return rc;
+  }
+  c->qwz_region = region;
   const size_t base = sym_offset + (c->qwz_uses++ & 1) * region;
   const size_t abs_off = align256((size_t)code_bytes(shard_len, bits, block));
   if (c->world == 1 && sec_out == nullptr && out_dtype == dtype) {
@@ -390,11 +420,13 @@ int zpp_hpz_allgather(zpp_comm_t c, size_t sym_offset, int64_t sec_len, int elem
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gather_copy_tma_kernel, 256, smem);
     const int64_t tiles = ceil_div(seg, kCopyTile) * n;
     const int grid = (int)std::min<int64_t>((int64_t)sm_count() * std::max(occ, 1), tiles);
-    gather_copy_tma_kernel<<<grid, 256, smem, st>>>(t, n, c->rank % c->group, seg, reinterpret_cast<uint8_t*>(out));
+    gather_copy_tma_kernel<<<grid, 256, smem, st>>>(t, n, c->rank % c->group, seg, reinterpret_cast<uint8_t*>(out),
+                                                    reinterpret_cast<const uint32_t*>(errflag));
     return check_cuda(cudaGetLastError(), "gather_copy_tma_kernel launch");
   }
   const int grid = (int)std::min<int64_t>(4 * sm_count(), std::max<int64_t>(1, ceil_div(seg * n, 16 * 256)));
-  gather_copy_kernel<<<grid, 256, 0, st>>>(t, n, c->rank % c->group, seg, reinterpret_cast<uint8_t*>(out), vec);
+  gather_copy_kernel<<<grid, 256, 0, st>>>(t, n, c->rank % c->group, seg, reinterpret_cast<uint8_t*>(out), vec,
+                                           reinterpret_cast<const uint32_t*>(errflag));
   return check_cuda(cudaGetLastError(), "gather_copy_kernel launch");
 }
 

@@ -27,6 +27,15 @@ __device__ __forceinline__ void raise_flag(uint32_t* flag, uint32_t bit) {
   if (flag) atomicOr(flag, bit);
 }
 
+// A device barrier of this flag's communicator timed out: the ranks' epochs
+// are out of step and peers' buffers may be stale or half written, so every
+// data kernel sharing the flag returns without touching its buffers until the
+// host clears the condition (Communicator.recover()).  One load per thread at
+// kernel entry.
+__device__ __forceinline__ bool comm_aborted(const uint32_t* flag) {
+  return flag && (*reinterpret_cast<const volatile uint32_t*>(flag) & FLAG_TIMEOUT);
+}
+
 // ---------------------------------------------------------------------------
 // exact helpers
 

@@ -494,6 +494,7 @@ template <typename T, int BITS, int LANES, int EPL, typename Addr, bool DEQ = fa
 __global__ void __launch_bounds__(256)
 quantize_reg_kernel(const T* __restrict__ x, Addr addr, int64_t n_blocks, uint8_t* __restrict__ codes,
                     float* __restrict__ absmax, uint32_t* __restrict__ flag, T* __restrict__ deq_out = nullptr) {
+  if (comm_aborted(flag)) return;
   static_assert(32 % LANES == 0 && EPL % 8 == 0, "team shape");
   constexpr int TPW = 32 / LANES;
   const int lane = threadIdx.x & 31;
@@ -556,6 +557,7 @@ template <typename T, typename Addr>
 __global__ void __launch_bounds__(256)
 absmax_generic_kernel(const T* __restrict__ x, Addr addr, int64_t n_chunks, int64_t B,
                       typename GenTraits<T>::Bits* __restrict__ absmax_bits, uint32_t* __restrict__ flag) {
+  if (comm_aborted(flag)) return;
   using Bits = typename GenTraits<T>::Bits;
   const int lane = threadIdx.x & 31;
   const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -789,6 +791,7 @@ __global__ void __launch_bounds__(256, 4)
 dequant16_kernel(SrcTable src, int n_src, int rot, int64_t shard_len, int64_t B, O* __restrict__ out,
                  O* __restrict__ sec_out, int64_t sec_lo, int64_t sec_len, int vec_ok, uint32_t* __restrict__ flag,
                  int64_t out_stride) {
+  if (comm_aborted(flag)) return;
   constexpr int E = Unit16B<BITS>::E;
   constexpr int U = BITS == 8 ? 2 : 1;  // 16-byte code loads per lane per tile
   constexpr int TU = 32 * U;            // units per warp tile
@@ -904,6 +907,7 @@ __global__ void __launch_bounds__(256)
 dequant16_tma_kernel(SrcTable src, int n_src, int rot, int64_t shard_len, int64_t B, O* __restrict__ out,
                      O* __restrict__ sec_out, int64_t sec_lo, int64_t sec_len, int vec_ok,
                      uint32_t* __restrict__ flag, int64_t out_stride) {
+  if (comm_aborted(flag)) return;
   constexpr int E = Unit16B<BITS>::E;
   constexpr int UPT = TILE_U / 256;  // units per thread per tile
   extern __shared__ __align__(128) uint8_t dsm[];  // [STAGES][TILE_U] uint4 ring, then STAGES mbarriers
@@ -1053,6 +1057,7 @@ __global__ void __launch_bounds__(256)
 dequant_gather_kernel(SrcTable src, int n_src, int rot, int64_t shard_len, int64_t B, O* __restrict__ out,
                       O* __restrict__ sec_out, int64_t sec_lo, int64_t sec_len, int vec_ok,
                       uint32_t* __restrict__ flag, int64_t out_stride) {
+  if (comm_aborted(flag)) return;
   constexpr int U = 4;
   using CW = typename std::conditional<BITS == 8, uint2, uint32_t>::type;
   const int lane = threadIdx.x & 31;
@@ -1107,6 +1112,7 @@ template <int BITS, typename A, typename O>
 __global__ void __launch_bounds__(256)
 dequant_reduce_kernel(SrcTable src, int n_src, int64_t n, int64_t B, O* __restrict__ out, double post_scale,
                       int vec_ok, uint32_t* __restrict__ flag) {
+  if (comm_aborted(flag)) return;
   constexpr int U = 2;
   constexpr int SB = 4;
   using CW = typename std::conditional<BITS == 8, uint2, uint32_t>::type;
@@ -1178,6 +1184,7 @@ template <int IBITS, typename IA, int OBITS, int LANES>
 __global__ void __launch_bounds__(256)
 drq_reg_kernel(SrcTable src, int n_src, int64_t n, int64_t B1, int64_t n_blocks_out, uint8_t* __restrict__ codes,
                double* __restrict__ absmax, uint32_t* __restrict__ flag) {
+  if (comm_aborted(flag)) return;
   constexpr int B2 = LANES * 16;
   constexpr int TPW = 32 / LANES;
   constexpr int QMAX = Codes<OBITS>::kQmax;
@@ -1386,6 +1393,7 @@ template <int BITS, typename A, typename O, bool VALIDATE>
 __global__ void __launch_bounds__(256)
 dequant_reduce16_kernel(SrcTable src, int n_src, int64_t n, int64_t B, O* __restrict__ out, double post_scale,
                         uint32_t* __restrict__ flag) {
+  if (comm_aborted(flag)) return;
   const int64_t units = n / 16;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const bool pow2 = (B & (B - 1)) == 0;
@@ -1496,6 +1504,7 @@ template <int IBITS, typename IA, int OBITS, int LANES, bool VALIDATE, typename 
 __global__ void __launch_bounds__(256)
 drq16_kernel(SrcTable src, int n_src, int64_t n, int64_t B1, int64_t n_blocks_out, uint8_t* __restrict__ codes,
              double* __restrict__ absmax, uint32_t* __restrict__ flag, FO* __restrict__ final_out = nullptr) {
+  if (comm_aborted(flag)) return;
   constexpr int TPW = 32 / LANES;
   const int lane = threadIdx.x & 31;
   const int tl = lane % LANES;
@@ -1534,6 +1543,7 @@ template <int IBITS, int OBITS, int NSRC, typename FO = void>
 __global__ void __launch_bounds__(256)
 drq_fast_kernel(SrcTable src, int64_t n, int lg1, int64_t n_blocks_out, uint8_t* __restrict__ codes,
                 double* __restrict__ absmax, uint32_t* __restrict__ flag, FO* __restrict__ final_out = nullptr) {
+  if (comm_aborted(flag)) return;
   using V = typename Vec16<IBITS>::T;
   constexpr int QMAX = Codes<OBITS>::kQmax;
   const int tl = threadIdx.x & 31;
@@ -1634,6 +1644,7 @@ drq_fast_kernel(SrcTable src, int64_t n, int lg1, int64_t n_blocks_out, uint8_t*
 template <int BITS, int NSRC, typename A, typename O>
 __global__ void __launch_bounds__(256)
 dr_fast_kernel(SrcTable src, int64_t n, int lg, O* __restrict__ out, double post_scale, uint32_t* __restrict__ flag) {
+  if (comm_aborted(flag)) return;
   using V = typename Vec16<BITS>::T;
   const int64_t units = n / 16;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -1744,6 +1755,7 @@ template <int IBITS, int OBITS, int NSRC, typename FO, int STAGES>
 __global__ void __launch_bounds__(256)
 drq_tma_kernel(SrcTable src, int64_t n, TmaTile tt, uint8_t* __restrict__ codes, double* __restrict__ absmax,
                uint32_t* __restrict__ flag, FO* __restrict__ final_out) {
+  if (comm_aborted(flag)) return;
   using V = typename Vec16<IBITS>::T;
   constexpr int UB = 2 * IBITS;
   constexpr int QMAX = Codes<OBITS>::kQmax;
@@ -1848,6 +1860,7 @@ drq_tma_kernel(SrcTable src, int64_t n, TmaTile tt, uint8_t* __restrict__ codes,
 template <int BITS, int NSRC, typename O, int STAGES>
 __global__ void __launch_bounds__(256)
 dr_tma_kernel(SrcTable src, int64_t n, TmaTile tt, O* __restrict__ out, uint32_t* __restrict__ flag) {
+  if (comm_aborted(flag)) return;
   using V = typename Vec16<BITS>::T;
   constexpr int UB = 2 * BITS;
   extern __shared__ __align__(128) uint8_t dsm[];

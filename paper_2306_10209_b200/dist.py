@@ -32,7 +32,7 @@ import torch
 import torch.distributed as dist
 
 from . import _lib
-from .errors import ValidationError
+from .errors import DeviceError, ValidationError
 from .partitioner import PartitionSpec
 from .quantizer import QuantConfig, device, dtype_code, stream_ptr
 
@@ -137,8 +137,18 @@ class Communicator:
         _lib.check(self.lib.zpp_comm_ipc_handle(h, mine), "zpp_comm_ipc_handle")
         allh = exchange_handles(mine.raw)
         buf = ctypes.create_string_buffer(allh, len(allh))
-        _lib.check(self.lib.zpp_comm_open_peers(h, buf), "zpp_comm_open_peers")
+        rc = self.lib.zpp_comm_open_peers(h, buf)
+        if rc != _lib.OK:
+            err = _lib.last_error()
+            self.lib.zpp_comm_destroy(h)
+            self.handle = None
+            raise DeviceError(
+                f"zpp_comm_open_peers: {err}. The fused collectives need every peer's symmetric buffer mapped "
+                "through CUDA IPC (cudaIpcOpenMemHandle), i.e. all ranks on one node with peer access between "
+                "their GPUs (NVLink/NVSwitch) and no container or driver policy blocking IPC. Use the NCCL "
+                "comparators (nccl_allgather / nccl_reduce_scatter) where that is not available.")
         self.flag = torch.zeros(1, dtype=torch.int32, device=device())
+        self._broken = False
         if hpz_sec:
             ptr = self.lib.zpp_comm_sym_ptr(h, self.rank) + self.layout.hpz
             self._secondary = _wrap_device(ptr, hpz_sec, hpz_dtype)
@@ -157,6 +167,7 @@ class Communicator:
 
         ``out_stride`` (elements between consecutive ranks' segments, default
         the shard length) lets a caller gather piece k of every shard in place."""
+        self._usable()
         n = int(shard.numel())
         if n > self.qwz_shard:
             raise ValidationError(f"shard has {n} elements, communicator was sized for {self.qwz_shard}")
@@ -232,6 +243,7 @@ class Communicator:
 
     def hpz_allgather(self, out: torch.Tensor | None = None) -> torch.Tensor:
         """hpZ: gather the group's secondary shards (member order) over NVLink."""
+        self._usable()
         if self._secondary is None:
             raise ValidationError("communicator has no hpZ secondary region")
         if out is None:
@@ -248,6 +260,7 @@ class Communicator:
                            out_dtype: torch.dtype = torch.float32, reorder: bool = True) -> torch.Tensor:
         """qgZ: this rank's partition (n/W elements) of the SUM over ranks,
         through two codec passes -- zs/collectives.py:464-569."""
+        self._usable()
         n = int(grad.numel())
         if n != self.qgz_elems:
             raise ValidationError(f"gradient has {n} elements, communicator was sized for {self.qgz_elems}")
@@ -285,13 +298,42 @@ class Communicator:
         _lib.check(self.lib.zpp_comm_barrier(self.handle, code, timeout_ms, self.flag.data_ptr(), stream_ptr()),
                    "barrier")
 
+    def _usable(self):
+        if self._broken:
+            raise DeviceError("communicator stopped after a device-barrier timeout; call recover() on every rank")
+
     def check(self):
         """Synchronise and raise the reference's exception for any device-side
-        condition seen since the last check (non-finite input, bad code, timeout)."""
+        condition seen since the last check (non-finite input, bad code, timeout).
+
+        The collectives are stream-ordered and host-asynchronous: their outputs
+        are only valid once check() has returned without raising.  After a
+        TIMEOUT (a peer never reached a device barrier) every later data kernel
+        on this communicator returns without touching its buffers, and the
+        communicator refuses new calls until recover() has run on every rank."""
         v = int(self.flag.item())
         if v:
-            self.flag.zero_()
+            if v & _lib.FLAG_TIMEOUT:
+                self._broken = True
+                self.flag.fill_(_lib.FLAG_TIMEOUT)
+            else:
+                self.flag.zero_()
             _lib.raise_for_flags(v, "zpp collective")
+
+    def recover(self):
+        """Collective re-initialisation after a barrier timeout: every rank
+        drains its device, passes a host barrier, restarts its barrier epochs
+        and double-buffer phases (zpp_comm_reset), clears its error word and
+        passes a second host barrier.  Then the communicator is usable again."""
+        torch.cuda.synchronize()
+        if dist.is_available() and dist.is_initialized():
+            dist.barrier()
+        _lib.check(self.lib.zpp_comm_reset(self.handle), "zpp_comm_reset")
+        self.flag.zero_()
+        torch.cuda.synchronize()
+        if dist.is_available() and dist.is_initialized():
+            dist.barrier()
+        self._broken = False
 
     def close(self):
         if getattr(self, "handle", None) is not None:
@@ -302,10 +344,20 @@ class Communicator:
             self.handle = None
 
     def __del__(self):
+        # Garbage collection is not collective: peers may still be pulling from
+        # this rank's symmetric buffer, so a multi-rank communicator that was
+        # never close()d is leaked (with a warning) instead of freed.
         try:
-            if getattr(self, "handle", None) is not None:
+            if getattr(self, "handle", None) is None:
+                return
+            if self.world == 1:
                 self.lib.zpp_comm_destroy(self.handle)
-                self.handle = None
+            else:
+                import warnings
+
+                warnings.warn("zpp Communicator garbage-collected without close(): its symmetric buffer is leaked "
+                              "(freeing it could fault peers still reading it)", ResourceWarning, stacklevel=2)
+            self.handle = None
         except Exception:
             pass
 

@@ -31,7 +31,7 @@ def _cases():
 @pytest.mark.parametrize("case", _cases(), ids=lambda c: c["name"])
 def test_training_run_matches_reference_bit_for_bit(case):
     import paper_2306_10209_b200 as zpp
-    from paper_2306_10209_b200 import engine as E
+    import engine_harness as E
 
     eng = E.TrainingEngine(E.ToyTaskConfig(**case["task"]), E.ZeroConfig(steps=case["steps"], **_cfg(zpp, case["zero"])))
     if case["passthrough"]:
@@ -53,7 +53,7 @@ def test_c08_passthrough_routing_is_bit_identical():
     import numpy as np
 
     import paper_2306_10209_b200 as zpp
-    from paper_2306_10209_b200 import engine as E
+    import engine_harness as E
 
     task = E.ToyTaskConfig()
     plain = E.TrainingEngine(task, E.ZeroConfig(steps=100))
@@ -68,7 +68,7 @@ def test_c08_passthrough_routing_is_bit_identical():
 
 def test_c09_convergence_envelope():
     import paper_2306_10209_b200 as zpp
-    from paper_2306_10209_b200 import engine as E
+    import engine_harness as E
 
     t0 = time.perf_counter()
     task = E.ToyTaskConfig(noise_sigma=0.1, input_scale_range=16.0)
@@ -95,7 +95,7 @@ def test_one_rank_run_equals_a_direct_adam_loop():
     masters) equals the same loop written out directly (zs/engine.py:332-428)."""
     import numpy as np
 
-    from paper_2306_10209_b200 import engine as E
+    import engine_harness as E
 
     task = E.ToyTaskConfig(**SMALL)
     cfg = E.ZeroConfig(nodes=1, gpus_per_node=1, steps=20, seed=11)
@@ -123,7 +123,7 @@ def test_one_rank_run_equals_a_direct_adam_loop():
 def test_hpz_moves_traffic_not_values():
     import numpy as np
 
-    from paper_2306_10209_b200 import engine as E
+    import engine_harness as E
 
     task = E.ToyTaskConfig(**SMALL)
     a = E.TrainingEngine(task, E.ZeroConfig(steps=8, seed=5))
@@ -136,7 +136,7 @@ def test_hpz_moves_traffic_not_values():
 
 def test_switch_volumes_and_schedule():
     import paper_2306_10209_b200 as zpp
-    from paper_2306_10209_b200 import engine as E
+    import engine_harness as E
 
     task = E.ToyTaskConfig(**SMALL)
     for s in E.train_toy(task, E.ZeroConfig(steps=3, seed=2)).steps:
@@ -156,7 +156,7 @@ def test_switch_volumes_and_schedule():
 
 
 def test_training_converges_and_divergence_is_flagged():
-    from paper_2306_10209_b200 import engine as E
+    import engine_harness as E
 
     task = E.ToyTaskConfig(**SMALL)
     rec = E.train_toy(task, E.ZeroConfig(steps=150, seed=7, lr=5e-3, quantized_weight_gather=True,

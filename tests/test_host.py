@@ -168,7 +168,7 @@ def test_secondary_gather_stays_on_node():
 def test_engine_mlp_gradient_matches_central_differences():
     """The toy engine's analytic MLP gradient (zs/engine.py:196-220, checked
     there by gradient_check :223-243) against central differences."""
-    from paper_2306_10209_b200 import engine as E
+    import engine_harness as E
 
     rng = np.random.default_rng(0)
     dims = [4, 5, 3]
@@ -185,11 +185,12 @@ def test_engine_mlp_gradient_matches_central_differences():
 
 
 def test_engine_config_validation():
+    import engine_harness as E
     import paper_2306_10209_b200 as zpp
 
     for kw in (dict(nodes=0), dict(steps=0), dict(lr=0.0), dict(grad_quant_fraction=1.5), dict(grad_stages=0)):
         with pytest.raises(zpp.ValidationError):
-            zpp.ZeroConfig(**kw)
+            E.ZeroConfig(**kw)
 
 
 def test_c10_latency_pipeline_model():
@@ -252,7 +253,7 @@ def test_engine_parts_on_the_host():
     batch, the input-scale ramp, and the up-front codec check
     (pkg/tests/test_engine.py restated)."""
     import paper_2306_10209_b200 as zpp
-    from paper_2306_10209_b200 import engine as E
+    import engine_harness as E
 
     flat = np.zeros(E.param_count([3, 4, 2]))
     (w0, _), (_, b1) = E._layers(flat, [3, 4, 2])
