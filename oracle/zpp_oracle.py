@@ -265,6 +265,35 @@ def qgz_2hop(inputs, x: int, y: int, s: int, inter_bits: int, inter_block: int,
     return (outs, hops) if return_hops else outs
 
 
+def qgz_2hop_slices(src, x: int, y: int, inter_bits: int, inter_block: int,
+                    intra_bits: int | None = None, intra_block: int | None = None) -> np.ndarray:
+    """One rank's qgZ output at sampled positions, from the W source ranks'
+    inputs at the same positions (zs/collectives.py:464-569 with reordering on,
+    restated through SURVEY Appendix A's index map).
+
+    Rank r's output element ``st*L + e`` is
+    ``fold_c'( dequant( requant_inter( fold_j'( dequant( quant_intra(
+    grad_{c'*X + j'}[r*S*L + st*L + e] ))))))`` -- folds from +0.0 in ascending
+    j' (local source) and c' (group).  Quantization blocks tile the slice
+    grid, so ``src`` (shape (W, K)) may concatenate any number of sampled
+    slices as long as each is a whole number of intra and inter blocks and
+    block-aligned in the output partition.  Checked against qgz_2hop in
+    tests/test_synth.py."""
+    intra_bits = inter_bits if intra_bits is None else intra_bits
+    intra_block = inter_block if intra_block is None else intra_block
+    src = np.asarray(src, dtype=np.float64)
+    k = src.shape[1]
+    out = np.zeros(k, dtype=np.float64)
+    for c in range(y):
+        acc = np.zeros(k, dtype=np.float64)
+        for j in range(x):
+            codes, scales, _ = quantize(src[c * x + j], intra_bits, intra_block)
+            acc += dequantize(codes, scales, k, intra_bits, intra_block)
+        codes, scales, _ = quantize(acc, inter_bits, inter_block)
+        out += dequantize(codes, scales, k, inter_bits, inter_block)
+    return out
+
+
 # ---------------------------------------------------------------------------
 # multi-threaded drivers for the CPU baseline (bench.py only)
 

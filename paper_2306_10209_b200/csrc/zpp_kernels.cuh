@@ -1539,13 +1539,72 @@ __device__ __forceinline__ double div_q_f32(float m) {
   return __fma_rn(e, r, q0);
 }
 
+// K2 epilogue for one 512-element output block b held by a warp (lane tl owns
+// elements e0 .. e0+15): the exact f64 block absmax (stored in f64), then
+// either the requantized codes (inactive lanes write the zero padding of a
+// partial last block, zs/quantizer.py:215-217) or, when hop 2 is a self-send
+// (FO != void), K3's fold of that one source rounded once to FO.
+template <int OBITS, typename FO>
+__device__ __forceinline__ void drq_epilogue(const double (&acc)[16], int64_t b, int tl, int64_t e0, bool active,
+                                             int64_t u, uint8_t* __restrict__ codes, double* __restrict__ absmax,
+                                             uint32_t* __restrict__ flag, FO* __restrict__ final_out) {
+  constexpr int QMAX = Codes<OBITS>::kQmax;
+  double mx = 0.0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) mx = dmax_nn(mx, fabs(acc[i]));
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) mx = dmax_nn(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+  if (tl == 0) {
+    absmax[b] = mx;
+    if (!(mx <= DBL_MAX)) raise_flag(flag, FLAG_NONFINITE);
+  }
+  const double inv = mx > 0.0 ? __ddiv_rn((double)QMAX, mx) : 0.0;
+  // r = RN(acc*inv) + 2^52+2^51: its low word is rint-even(acc*inv) (|.| <= qmax,
+  // no clamp needed) and r - (2^52+2^51) is that code as an exact double
+  double r[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) r[i] = __dadd_rn(__dmul_rn(acc[i], inv), kMagic52);
+  if constexpr (std::is_void<FO>::value) {
+    uint32_t q0[8], q1[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      q0[i] = (uint32_t)__double2loint(r[i]);
+      q1[i] = (uint32_t)__double2loint(r[8 + i]);
+    }
+    // inactive lanes hold zeros: they write the zero padding of a partial
+    // last block (zs/quantizer.py:215-217)
+    uint8_t* dst = codes + u * 2 * OBITS;
+    if constexpr (OBITS == 8) {
+      const uint2 a = pack8_int8(q0), c = pack8_int8(q1);
+      *reinterpret_cast<uint4*>(dst) = make_uint4(a.x, a.y, c.x, c.y);
+    } else {
+      *reinterpret_cast<uint2*>(dst) = make_uint2(pack8_int4(q0), pack8_int4(q1));
+    }
+  } else if (active) {
+    // hop 2 to itself: K3's fold of one source, RN(+0.0 + RN(code*s2)) = RN(code*s2)
+    const double s2 = scale_of<OBITS>(mx);
+    double v[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __dmul_rn(__dsub_rn(r[i], kMagic52), s2);
+    FO* dst = final_out + e0;
+    if constexpr (sizeof(FO) == 4) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        reinterpret_cast<float4*>(dst)[i] = make_float4(from_f64<float>(v[4 * i]), from_f64<float>(v[4 * i + 1]),
+                                                        from_f64<float>(v[4 * i + 2]), from_f64<float>(v[4 * i + 3]));
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) reinterpret_cast<double2*>(dst)[i] = make_double2(v[2 * i], v[2 * i + 1]);
+    }
+  }
+}
+
 template <int IBITS, int OBITS, int NSRC, typename FO = void>
 __global__ void __launch_bounds__(256)
 drq_fast_kernel(SrcTable src, int64_t n, int lg1, int64_t n_blocks_out, uint8_t* __restrict__ codes,
                 double* __restrict__ absmax, uint32_t* __restrict__ flag, FO* __restrict__ final_out = nullptr) {
   if (comm_aborted(flag)) return;
   using V = typename Vec16<IBITS>::T;
-  constexpr int QMAX = Codes<OBITS>::kQmax;
   const int tl = threadIdx.x & 31;
   const int64_t nwarp = ((int64_t)gridDim.x * blockDim.x) >> 5;
   bool bad = false;
@@ -1584,54 +1643,129 @@ drq_fast_kernel(SrcTable src, int64_t n, int lg1, int64_t n_blocks_out, uint8_t*
     fold16<IBITS, true, true>(w[0], div_q_f32<Codes<IBITS>::kQmax>(m[0]), acc, bad);
 #pragma unroll
     for (int j = 1; j < NSRC; ++j) fold16<IBITS, true>(w[j], div_q_f32<Codes<IBITS>::kQmax>(m[j]), acc, bad);
-    double mx = 0.0;
+    drq_epilogue<OBITS, FO>(acc, b, tl, e0, active, u, codes, absmax, flag, final_out);
+  }
+  if (bad) raise_flag(flag, FLAG_BADCODE);
+}
+
+// ---------------------------------------------------------------------------
+// Product tables for INT4 folds.  The reference's fold step adds RN64(c * s)
+// for a code c in [-7, 7] and its block scale s (zs/quantizer.py:237,
+// :255-257; zs/collectives.py:71-75): 15 possible products per (source,
+// block).  When one block scale covers a whole warp's 512 elements, the warp
+// computes them once into shared memory --
+//     T[c + 8] = RN64(+0.0 + RN64(c * s))
+// (the +0.0 turns the -0.0 product of a negative code with s == 0 into the
+// +0.0 that the reference's fold from +0.0 produces; the fold never holds
+// -0.0, so adding +0.0 instead of -0.0 later is the same) -- and each code then
+// costs one PRMT (its byte offset into the table), one LDS.64 and one DADD,
+// instead of fold16's PRMT + MOV + DSUB + DMUL + DADD.  Same products, same
+// fold order: the same bits.  A table is 16 doubles = 128 contiguous bytes, so
+// any mix of lanes' entries touches each of the 32 banks at most once.
+
+// Table layout: one 256-byte-aligned slot per (warp, source), entries at the
+// slot start, so the shared address of entry k is one PRMT: the slot address
+// with its low byte replaced by 8k (8k <= 120) -- no address add per code.
+constexpr int kTblSlotDoubles = 32;  // 256 bytes
+
+// lanes 16*h .. 16*h+15 build source 2p+h's table (entry lane & 15) from the
+// block absmax m[j] (identical in every lane): one scale division and one
+// product per lane per pass
+template <int NSRC, typename A>
+__device__ __forceinline__ void tbl4_build(double* __restrict__ tbl, const A (&m)[NSRC], int lane) {
 #pragma unroll
-    for (int i = 0; i < 16; ++i) mx = dmax_nn(mx, fabs(acc[i]));
-#pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) mx = dmax_nn(mx, __shfl_xor_sync(0xffffffffu, mx, off));
-    if (tl == 0) {
-      absmax[b] = mx;
-      if (!(mx <= DBL_MAX)) raise_flag(flag, FLAG_NONFINITE);
+  for (int p = 0; p < (NSRC + 1) / 2; ++p) {
+    const int h = lane >> 4;
+    const int j = 2 * p + h;
+    const A mj = h ? m[2 * p + 1 < NSRC ? 2 * p + 1 : 2 * p] : m[2 * p];
+    if (j < NSRC) {
+      double sj;
+      if constexpr (sizeof(A) == 4) sj = div_q_f32<7>(mj);
+      else sj = scale_of<4>(mj);
+      tbl[j * kTblSlotDoubles + (lane & 15)] = __dadd_rn(0.0, __dmul_rn((double)((lane & 15) - 8), sj));
     }
-    const double inv = mx > 0.0 ? __ddiv_rn((double)QMAX, mx) : 0.0;
-    // r = RN(acc*inv) + 2^52+2^51: its low word is rint-even(acc*inv) (|.| <= qmax,
-    // no clamp needed) and r - (2^52+2^51) is that code as an exact double
-    double r[16];
+  }
+}
+
+__device__ __forceinline__ double lds_f64(uint32_t addr) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr) : "memory");
+  return v;
+}
+
+// acc[i] (+)= T[code_i + 8] for the 16 INT4 codes in w (element order as
+// fold16); `slot` = shared address of the source's table (256-byte aligned)
+template <bool ASSIGN>
+__device__ __forceinline__ void fold16_tbl4(const uint2& w, uint32_t slot, double (&acc)[16], bool& bad) {
+  const uint32_t ww[2] = {w.x, w.y};
 #pragma unroll
-    for (int i = 0; i < 16; ++i) r[i] = __dadd_rn(__dmul_rn(acc[i], inv), kMagic52);
-    if constexpr (std::is_void<FO>::value) {
-      uint32_t q0[8], q1[8];
+  for (int k = 0; k < 2; ++k) {
+    bad |= has_nibble_8(ww[k]);
+    const uint32_t b = ww[k] ^ 0x88888888u;     // biased nibbles c + 8
+    const uint32_t ev = (b << 3) & 0x78787878u;  // 8 * (low nibble) in each byte
+    const uint32_t od = (b >> 1) & 0x78787878u;  // 8 * (high nibble) in each byte
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        q0[i] = (uint32_t)__double2loint(r[i]);
-        q1[i] = (uint32_t)__double2loint(r[8 + i]);
-      }
-      // inactive lanes hold zeros: they write the zero padding of a partial
-      // last block (zs/quantizer.py:215-217)
-      uint8_t* dst = codes + u * 2 * OBITS;
-      if constexpr (OBITS == 8) {
-        const uint2 a = pack8_int8(q0), c = pack8_int8(q1);
-        *reinterpret_cast<uint4*>(dst) = make_uint4(a.x, a.y, c.x, c.y);
+    for (int j = 0; j < 4; ++j) {
+      const double v0 = lds_f64(__byte_perm(ev, slot, 0x7650 + j));
+      const double v1 = lds_f64(__byte_perm(od, slot, 0x7650 + j));
+      if constexpr (ASSIGN) {
+        acc[8 * k + 2 * j] = v0;
+        acc[8 * k + 2 * j + 1] = v1;
       } else {
-        *reinterpret_cast<uint2*>(dst) = make_uint2(pack8_int4(q0), pack8_int4(q1));
-      }
-    } else if (active) {
-      // hop 2 to itself: K3's fold of one source, RN(+0.0 + RN(code*s2)) = RN(code*s2)
-      const double s2 = scale_of<OBITS>(mx);
-      double v[16];
-#pragma unroll
-      for (int i = 0; i < 16; ++i) v[i] = __dmul_rn(__dsub_rn(r[i], kMagic52), s2);
-      FO* dst = final_out + e0;
-      if constexpr (sizeof(FO) == 4) {
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-          reinterpret_cast<float4*>(dst)[i] = make_float4(from_f64<float>(v[4 * i]), from_f64<float>(v[4 * i + 1]),
-                                                          from_f64<float>(v[4 * i + 2]), from_f64<float>(v[4 * i + 3]));
-      } else {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) reinterpret_cast<double2*>(dst)[i] = make_double2(v[2 * i], v[2 * i + 1]);
+        acc[8 * k + 2 * j] = __dadd_rn(acc[8 * k + 2 * j], v0);
+        acc[8 * k + 2 * j + 1] = __dadd_rn(acc[8 * k + 2 * j + 1], v1);
       }
     }
+  }
+}
+
+// K2 with INT4 sources through product tables (the qgZ hop-1 reduce with the
+// INT4/512 intra codec): as drq_fast_kernel, for input blocks that are
+// multiples of 512 (one scale per warp and source).  Every lane loads the
+// block absmax even past the end of a partial last block, so the table inputs
+// are warp-uniform.
+template <int OBITS, int NSRC, typename FO = void>
+__global__ void __launch_bounds__(256)
+drq_tbl_kernel(SrcTable src, int64_t n, int lg1, int64_t n_blocks_out, uint8_t* __restrict__ codes,
+               double* __restrict__ absmax, uint32_t* __restrict__ flag, FO* __restrict__ final_out = nullptr) {
+  if (comm_aborted(flag)) return;
+  __shared__ __align__(256) double tbl_all[8][NSRC * kTblSlotDoubles];
+  const int tl = threadIdx.x & 31;
+  double* tbl = tbl_all[threadIdx.x >> 5];
+  const uint32_t slot0 = (uint32_t)__cvta_generic_to_shared(tbl);
+  const int64_t nwarp = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  bool bad = false;
+  uint2 w[NSRC], wn[NSRC];
+  float m[NSRC], mn[NSRC];
+  auto load = [&](int64_t b, uint2 (&wv)[NSRC], float (&mv)[NSRC]) {
+    const int64_t e0 = b * 512 + (int64_t)tl * 16;
+    const bool blk = b < n_blocks_out, ok = blk && e0 < n;
+#pragma unroll
+    for (int j = 0; j < NSRC; ++j) {
+      wv[j] = ok ? __ldg(reinterpret_cast<const uint2*>(src.codes[j]) + (e0 >> 4)) : make_uint2(0, 0);
+      mv[j] = blk ? __ldg(reinterpret_cast<const float*>(src.absmax[j]) + ((b * 512) >> lg1)) : 0.0f;
+    }
+  };
+  int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  load(b, wn, mn);
+  for (; b < n_blocks_out; b += nwarp) {
+    const int64_t e0 = b * 512 + (int64_t)tl * 16;
+    const bool active = e0 < n;
+    const int64_t u = e0 >> 4;
+#pragma unroll
+    for (int j = 0; j < NSRC; ++j) {
+      w[j] = wn[j];
+      m[j] = mn[j];
+    }
+    load(b + nwarp, wn, mn);
+    __syncwarp();  // the previous block's lookups are done before the tables change
+    tbl4_build<NSRC>(tbl, m, tl);
+    __syncwarp();
+    double acc[16];
+    fold16_tbl4<true>(w[0], slot0, acc, bad);
+#pragma unroll
+    for (int j = 1; j < NSRC; ++j) fold16_tbl4<false>(w[j], slot0 + j * 256, acc, bad);
+    drq_epilogue<OBITS, FO>(acc, b, tl, e0, active, u, codes, absmax, flag, final_out);
   }
   if (bad) raise_flag(flag, FLAG_BADCODE);
 }

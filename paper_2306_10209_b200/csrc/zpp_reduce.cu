@@ -106,12 +106,29 @@ static bool drq_fast_ok(int n_src, int64_t n, int64_t in_block, int64_t out_bloc
          (in_block & (in_block - 1)) == 0 && (n_src == 1 || n_src == 2 || n_src == 4 || n_src == 8);
 }
 
+// ZPP_NO_TBL=1 (development A/B only): INT4 folds without product tables
+bool tbl_off() {
+  static const bool off = [] {
+    const char* e = getenv("ZPP_NO_TBL");
+    return e && e[0] == '1';
+  }();
+  return off;
+}
+
 template <int IBITS, int OBITS, typename FO>
 static int run_drq_fast(const SrcTable& t, int n_src, int64_t n, int64_t in_block, int64_t nbo, uint8_t* codes,
                         double* absmax, FO* final_out, uint32_t* flag, cudaStream_t st) {
   const int lg1 = __builtin_ctzll((unsigned long long)in_block);
+  // INT4 sources with one scale per 512-element warp tile: product tables
+  const bool tbl = IBITS == 4 && in_block % 512 == 0 && !tbl_off();
 #define ZPP_FAST(NS)                                                                            \
   {                                                                                             \
+    if (tbl) {                                                                                  \
+      auto k = drq_tbl_kernel<OBITS, NS, FO>;                                                   \
+      const int grid = grid_for(k, 256, ceil_div(nbo, 8));                                      \
+      k<<<grid, 256, 0, st>>>(t, n, lg1, nbo, codes, absmax, flag, final_out);                  \
+      return check_cuda(cudaGetLastError(), "drq_tbl_kernel launch");                           \
+    }                                                                                           \
     auto k = drq_fast_kernel<IBITS, OBITS, NS, FO>;                                             \
     const int grid = grid_for(k, 256, ceil_div(nbo, 8));                                        \
     k<<<grid, 256, 0, st>>>(t, n, lg1, nbo, codes, absmax, flag, final_out);                    \

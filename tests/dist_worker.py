@@ -25,6 +25,14 @@ def bf16_bits(v):
     return (np.asarray(v, np.float32).view(np.uint32) >> 16).astype(np.uint16)
 
 
+def same_bits(a, b):
+    """Bitwise equality (np.array_equal would accept -0.0 for +0.0)."""
+    a, b = np.asarray(a), np.asarray(b)
+    if a.shape != b.shape or a.dtype != b.dtype:
+        return False
+    return bool(np.array_equal(a.view(f"u{a.dtype.itemsize}"), b.view(f"u{b.dtype.itemsize}")))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--group", type=int, default=2)
@@ -67,26 +75,56 @@ def main():
     for it in range(3):  # exercise both halves of the double buffer
         out = comm.qwz_allgather(mine, write_secondary=True)
         comm.check()
-        check(f"qwz it{it}", np.array_equal(out.cpu().numpy(), want16))
-        check(f"hpz secondary it{it}", np.array_equal(comm.secondary.cpu().numpy(), want16[lo:hi]))
+        check(f"qwz it{it}", same_bits(out.cpu().numpy(), want16))
+        check(f"hpz secondary it{it}", same_bits(comm.secondary.cpu().numpy(), want16[lo:hi]))
         g = comm.hpz_allgather()
         comm.check()
-        check(f"hpz gather it{it}", np.array_equal(g.cpu().numpy(), want16))
+        check(f"hpz gather it{it}", same_bits(g.cpu().numpy(), want16))
     # host-buffer API with transfer/compute overlap (chunked sub-collectives)
     h_in = torch.from_numpy(shards[rank]).pin_memory()
     h_out = torch.empty(total, dtype=torch.float16).pin_memory()
     comm.qwz_allgather_host(h_in, h_out, chunks=3)
     torch.cuda.synchronize()
     comm.check()
-    check("qwz host chunked", np.array_equal(h_out.numpy(), want16))
+    check("qwz host chunked", same_bits(h_out.numpy(), want16))
     # f32 output of the same gather
     out32 = comm.qwz_allgather(mine, out_dtype=torch.float32)
     comm.check()
-    check("qwz fp32", np.array_equal(out32.cpu().numpy(), want.astype(np.float32)))
+    check("qwz fp32", same_bits(out32.cpu().numpy(), want.astype(np.float32)))
+    # back-to-back calls with different shard lengths and no host sync in
+    # between: the half boundaries of the qwZ double buffer move, so K0 of a
+    # call must not overwrite codes peers still pull for the previous one
+    lens = [shard_len, 4096, shard_len, 2048 + 512, 1024, shard_len, 4096]
+    outs = [comm.qwz_allgather(mine[:m]) for m in lens]
+    comm.check()
+    for i, m in enumerate(lens):
+        wm, _ = O.all_gather_qwz([s[:m].astype(np.float64) for s in shards], 8, 2048)
+        check(f"qwz varying length #{i} ({m})", same_bits(outs[i].cpu().numpy(), wm.astype(np.float16)))
+    # a device barrier that times out: this rank's data kernels stop, the
+    # communicator refuses further calls, and recover() (collective) restores it
+    if rank == 0:
+        comm.barrier("world", timeout_ms=200)  # the other ranks never arrive
+        try:
+            comm.check()
+            check("timeout raised", False)
+        except zpp.DeviceError:
+            pass
+        try:
+            comm.qwz_allgather(mine)
+            check("broken communicator refuses calls", False)
+        except zpp.DeviceError:
+            pass
+    comm.recover()
+    out = comm.qwz_allgather(mine, write_secondary=True)
+    comm.check()
+    check("qwz after recover", same_bits(out.cpu().numpy(), want16))
+    g = comm.hpz_allgather()
+    comm.check()
+    check("hpz after recover", same_bits(g.cpu().numpy(), want16))
     # NCCL comparator gathers the raw shards
     if not oversub:
         raw = nccl_allgather(mine)
-        check("nccl allgather", np.array_equal(raw.cpu().numpy(), np.concatenate(shards)))
+        check("nccl allgather", same_bits(raw.cpu().numpy(), np.concatenate(shards)))
 
     # ---- qgZ -----------------------------------------------------------------
     n = args.stages * world * 1024
@@ -97,10 +135,10 @@ def main():
     for it in range(3):
         o64 = comm.qgz_reduce_scatter(gt, out_dtype=torch.float64)
         comm.check()
-        check(f"qgz f64 it{it}", np.array_equal(o64.cpu().numpy(), ref))
+        check(f"qgz f64 it{it}", same_bits(o64.cpu().numpy(), ref))
         o32 = comm.qgz_reduce_scatter(gt)
         comm.check()
-        check(f"qgz f32 it{it}", np.array_equal(o32.cpu().numpy(), ref.astype(np.float32)))
+        check(f"qgz f32 it{it}", same_bits(o32.cpu().numpy(), ref.astype(np.float32)))
     # a second communicator and bucket size: 83 blocks per slice, stages 1
     L2 = 2 * 16384 + 17 * 512
     n2 = world * L2
@@ -111,7 +149,7 @@ def main():
     for it in range(3):
         o2 = comm2.qgz_reduce_scatter(gt2, out_dtype=torch.float64)
         comm2.check()
-        check(f"qgz bucket2 it{it}", np.array_equal(o2.cpu().numpy(), ref2))
+        check(f"qgz bucket2 it{it}", same_bits(o2.cpu().numpy(), ref2))
     comm2.close()
     # ---- process groups for the staged comparators ---------------------------
     mine_pg, cross_pg = make_groups(X)

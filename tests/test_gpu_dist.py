@@ -20,12 +20,19 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _run(nproc, group, stages, env=None):
+def _run(nproc, group, stages, env=None, worker="dist_worker.py", extra=()):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
-           os.path.join(HERE, "dist_worker.py"), "--group", str(group), "--stages", str(stages)]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env={**os.environ, **(env or {})})
+           os.path.join(HERE, worker), "--group", str(group), *(["--stages", str(stages)] if stages else []), *extra]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env={**os.environ, **(env or {})})
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
+    return r.stdout
+
+
+def _run_large(nproc, group, env=None):
+    """BASELINE shapes with sampled bitwise parity (tests/dist_large_worker.py)."""
+    out = _run(nproc, group, 0, env=env, worker="dist_large_worker.py")
+    assert "large parity ok" in out, out[-4000:]
 
 
 @pytest.mark.parametrize("group", [1, 2])
@@ -60,3 +67,34 @@ def test_eight_ranks_2x4_oversubscribed():
     if n < 2 or n >= 8:
         pytest.skip("needs 2..7 GPUs (8 run test_eight_gpus_2x4)")
     _run(8, 4, 1, env={"ZPP_OVERSUBSCRIBE": "1"})
+
+
+# ---- the BASELINE shapes: 1.3B qwZ, 256 MiB qgZ bucket, GPT-13B layer ---------
+
+
+@pytest.mark.parametrize("group", [1, 2])
+def test_large_two_gpus(group):
+    _run_large(2, group)
+
+
+@pytest.mark.parametrize("group", [4, 2])
+def test_large_four_gpus(group):
+    """1x4 and 2x2 at the BASELINE shapes."""
+    if torch.cuda.device_count() < 4:
+        pytest.skip("needs 4 GPUs")
+    _run_large(4, group)
+
+
+def test_large_eight_gpus_2x4():
+    if torch.cuda.device_count() < 8:
+        pytest.skip("needs 8 GPUs")
+    _run_large(8, 4)
+
+
+def test_large_eight_ranks_2x4_oversubscribed():
+    """The 2x4 layout at the BASELINE shapes, two ranks per GPU (see
+    test_eight_ranks_2x4_oversubscribed)."""
+    n = torch.cuda.device_count()
+    if n < 4 or n >= 8:
+        pytest.skip("needs 4..7 GPUs (8 run test_large_eight_gpus_2x4)")
+    _run_large(8, 4, env={"ZPP_OVERSUBSCRIBE": "1"})
