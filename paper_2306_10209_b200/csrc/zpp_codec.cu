@@ -185,6 +185,63 @@ int launch_quantize(const void* x, int dtype, const AddrSpec& a, int64_t n_out, 
   return quantize_dispatch(x, dtype, addr, n_out, bits, block, codes, absmax, flag, st);
 }
 
+// K1 with the hop-1 push (quantize_push_kernel): register-path blocks only
+template <typename T, int BITS, int LANES, int EPL = Raw<T>::kEPL>
+static int run_qpush(const T* x, const SwizzleAddr& addr, int n_msg, int first, const PushDst& dst, uint32_t* flag,
+                     cudaStream_t st) {
+  auto k = quantize_push_kernel<T, BITS, LANES, EPL>;
+  const int64_t tiles = ceil_div((int64_t)dst.mb.d, PushTile<LANES, EPL, BITS>::WT) * n_msg;
+  const int grid = grid_for(k, 256, ceil_div(tiles, 8));
+  k<<<grid, 256, 0, st>>>(x, addr, n_msg, first, dst, flag);
+  return check_cuda(cudaGetLastError(), "quantize_push_kernel launch");
+}
+
+template <typename T, int BITS>
+static int dispatch_qpush(const T* x, const SwizzleAddr& addr, int n_msg, int first, int64_t block,
+                          const PushDst& dst, uint32_t* flag, cudaStream_t st, bool* handled) {
+  *handled = true;
+  constexpr int64_t EPL = Raw<T>::kEPL;
+  // LANES >= 2 keeps every block's codes a 16-byte multiple (INT4, 16-bit input)
+  if (block == 2 * EPL) return run_qpush<T, BITS, 2>(x, addr, n_msg, first, dst, flag, st);
+  if (block == 4 * EPL) return run_qpush<T, BITS, 4>(x, addr, n_msg, first, dst, flag, st);
+  if (block == 8 * EPL) return run_qpush<T, BITS, 8>(x, addr, n_msg, first, dst, flag, st);
+  if (block == 16 * EPL) return run_qpush<T, BITS, 16>(x, addr, n_msg, first, dst, flag, st);
+  if (block == 32 * EPL) return run_qpush<T, BITS, 32>(x, addr, n_msg, first, dst, flag, st);
+  *handled = false;
+  return ZPP_OK;
+}
+
+int launch_quantize_push(const void* x, int dtype, const AddrSpec& a, int64_t n_out, int bits, int64_t block,
+                         uint8_t* const* dst_codes, uint8_t* const* dst_absmax, int64_t msg_blocks, int first,
+                         uint32_t* flag, cudaStream_t st, bool* handled) {
+  *handled = false;
+  if (n_out == 0 || !a.swizzle || !aligned16(x) || a.X > kMaxPush) return ZPP_OK;
+  if (a.L / block >= (1ll << 31) || (int64_t)a.X * a.Y * (a.L / block) >= (1ll << 31)) return ZPP_OK;
+  for (int j = 0; j < a.X; ++j)
+    if (!aligned16(dst_codes[j])) return ZPP_OK;
+  SwizzleAddr addr{a.L, a.part, a.stage_off, block, a.X, a.Y, a.reorder,
+                   FastDiv::make((uint32_t)(a.L / block)), FastDiv::make((uint32_t)a.Y)};
+  PushDst d;
+  for (int j = 0; j < kMaxPush; ++j) {
+    d.codes[j] = j < a.X ? dst_codes[j] : nullptr;
+    d.absmax[j] = j < a.X ? dst_absmax[j] : nullptr;
+  }
+  d.mb = FastDiv::make((uint32_t)msg_blocks);
+  if (ceil_div(n_out, block) != (int64_t)a.X * msg_blocks) return fail(ZPP_ERR_VALIDATION, "push: bad message size");
+  const auto* xx = x;
+#define ZPP_P(T)                                                                                                 \
+  return bits == 8                                                                                               \
+             ? dispatch_qpush<T, 8>(reinterpret_cast<const T*>(xx), addr, a.X, first, block, d, flag, st, handled) \
+             : dispatch_qpush<T, 4>(reinterpret_cast<const T*>(xx), addr, a.X, first, block, d, flag, st, handled);
+  switch (dtype) {
+    case ZPP_F32: ZPP_P(float)
+    case ZPP_F16: ZPP_P(__half)
+    case ZPP_BF16: ZPP_P(__nv_bfloat16)
+  }
+#undef ZPP_P
+  return ZPP_OK;
+}
+
 // ---------------------------------------------------------------------------
 // K4 gather-dequantize and K3 dequant-reduce
 

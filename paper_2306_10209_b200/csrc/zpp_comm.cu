@@ -515,6 +515,32 @@ int zpp_qgz_reduce_scatter(zpp_comm_t c, size_t sym_offset, const void* grad, in
     return e ? atoi(e) : 0;
   }();
   const int k1_sms = pipelined ? (k1_sms_env > 0 ? k1_sms_env : sm_count() / 3) : 0;
+  // Hop 1 either
+  //  * push: K1 (quantize_push_kernel) streams each message into the receiving
+  //    peer's [src_loc][c][e] region with TMA bulk stores while it quantizes,
+  //    and K2 folds local HBM; or
+  //  * pull: K1 writes the local send buffer and K2 (drq_tma_kernel) pulls the
+  //    X messages over NVLink while it folds.
+  // Measured on 4 B200s (profiles/r2/qgz_push_pull_r2.md), 256 MiB bf16
+  // bucket: 2x2 push 237 us vs pull 246 us; 1x4 push 195 us vs pull 187 us
+  // (with one group K2 also writes the fp32 partition, and its NVLink pull
+  // hides under that work), so push is used when there is a second hop
+  // (Y > 1) and K1 has a register path.  ZPP_QGZ_MODE=push|pull overrides
+  // (development A/B).  The choice depends only on arguments every rank shares.
+  const size_t msg_code_bytes = (size_t)code_bytes(msg_elems, intra_bits, intra_block);
+  const int64_t msg_blocks = msg_elems / intra_block;
+  static const int mode_env = [] {
+    const char* e = getenv("ZPP_QGZ_MODE");
+    if (!e) e = getenv("ZPP_QGZ_PULL") && getenv("ZPP_QGZ_PULL")[0] == '1' ? "pull" : nullptr;
+    return !e ? 0 : (e[1] == 'u' && e[2] == 's') ? 1 : 2;  // 1 push, 2 pull
+  }();
+  const int64_t epl = dtype == ZPP_F32 ? 32 : 64;
+  const bool want_push = mode_env == 1 || (mode_env == 0 && Y > 1);
+  const bool push = want_push && dtype != ZPP_F64 && X <= 8 && intra_block % epl == 0 &&
+                    intra_block / epl >= 2 && intra_block / epl <= 32 &&
+                    ((intra_block / epl) & (intra_block / epl - 1)) == 0;
+  if (push && (reinterpret_cast<uintptr_t>(grad) & 15))
+    return fail(ZPP_ERR_VALIDATION, "qgZ: the gradient buffer must be 16-byte aligned");
   auto k1 = [&](int s, cudaStream_t on) {
     SmBudget budget(s > 0 ? k1_sms : 0);  // K1(0) runs alone
     AddrSpec a;
@@ -526,6 +552,22 @@ int zpp_qgz_reduce_scatter(zpp_comm_t c, size_t sym_offset, const void* grad, in
     a.Y = Y;
     a.reorder = reorder ? 1 : 0;
     const size_t base = base_of(s);
+    if (push) {
+      uint8_t* dc[kMaxPush];
+      uint8_t* da[kMaxPush];
+      for (int j = 0; j < X; ++j) {
+        uint8_t* p = c->peers[node * X + j] + base;
+        dc[j] = p + l.send_codes + msg_code_bytes * loc;
+        da[j] = p + l.send_abs + (size_t)msg_blocks * in_abs_sz * loc;
+      }
+      bool handled = false;
+      // rank loc starts with the message for local peer loc+1: the group's
+      // ranks begin on different destinations
+      const int rc1 = launch_quantize_push(grad, dtype, a, (int64_t)W * L, intra_bits, intra_block, dc, da, msg_blocks,
+                                           (loc + 1) % X, flag, on, &handled);
+      if (rc1 || handled) return rc1;
+      return fail(ZPP_ERR_VALIDATION, "qgZ: no push path for this shape");
+    }
     return launch_quantize(grad, dtype, a, (int64_t)W * L, intra_bits, intra_block, c->local + base + l.send_codes,
                            c->local + base + l.send_abs, flag, on);
   };
@@ -556,17 +598,24 @@ int zpp_qgz_reduce_scatter(zpp_comm_t c, size_t sym_offset, const void* grad, in
       if ((rc = check_cuda(cudaEventRecord(c->ev_k1, c->side), "record"))) return rc;
     }
     SmBudget budget(pipelined && s + 1 < stages ? sm_count() - k1_sms : 0);
-    // K2: pull message `loc` from every group member (ascending local rank)
+    // K2: the X messages for this rank, ascending local source -- pushed into
+    // this rank's receive region by the group's K1s, or pulled from the peers
     const void* codes[kMaxRanks];
     const void* absmax[kMaxRanks];
     for (int j = 0; j < X; ++j) {
-      const uint8_t* p = c->peers[node * X + j] + base;
-      codes[j] = p + l.send_codes + (size_t)code_bytes(msg_elems, intra_bits, intra_block) * loc;
-      absmax[j] = p + l.send_abs + (size_t)(msg_elems / intra_block) * in_abs_sz * loc;
+      if (push) {
+        const uint8_t* p = c->local + base;
+        codes[j] = p + l.send_codes + msg_code_bytes * j;
+        absmax[j] = p + l.send_abs + (size_t)msg_blocks * in_abs_sz * j;
+      } else {
+        const uint8_t* p = c->peers[node * X + j] + base;
+        codes[j] = p + l.send_codes + msg_code_bytes * loc;
+        absmax[j] = p + l.send_abs + (size_t)msg_blocks * in_abs_sz * loc;
+      }
     }
     if (Y == 1) {  // hop 2 is a self-send: K2 writes the final partition directly
       bool handled = false;
-      if (in_abs == ZPP_F32)
+      if (in_abs == ZPP_F32 && !push)
         rc = launch_drq_tma(codes, absmax, X, msg_elems, intra_bits, intra_block, inter_bits, inter_block, nullptr,
                             reinterpret_cast<double*>(c->local + base + l.hop_abs),
                             reinterpret_cast<uint8_t*>(out) + (size_t)s * L * out_esz, out_dtype, flag, st, &handled);
@@ -585,7 +634,7 @@ int zpp_qgz_reduce_scatter(zpp_comm_t c, size_t sym_offset, const void* grad, in
       }
     }
     bool handled = false;
-    if (in_abs == ZPP_F32)
+    if (in_abs == ZPP_F32 && !push)
       rc = launch_drq_tma(codes, absmax, X, msg_elems, intra_bits, intra_block, inter_bits, inter_block,
                           c->local + base + l.hop_codes, reinterpret_cast<double*>(c->local + base + l.hop_abs),
                           nullptr, 0, flag, st, &handled);

@@ -26,6 +26,13 @@ struct AddrSpec {
 // launchers (validated arguments)
 int launch_quantize(const void* x, int dtype, const AddrSpec& a, int64_t n_out, int bits, int64_t block,
                     uint8_t* codes, void* absmax, uint32_t* flag, cudaStream_t st);
+// K1 fused with the qgZ hop-1 push: message j of the send buffer (msg_blocks
+// blocks) goes to dst_codes[j] / dst_absmax[j] (fp32); tiles cycle through
+// the messages starting at `first`.  *handled = false when
+// the shape has no push path (the caller then quantizes locally).
+int launch_quantize_push(const void* x, int dtype, const AddrSpec& a, int64_t n_out, int bits, int64_t block,
+                         uint8_t* const* dst_codes, uint8_t* const* dst_absmax, int64_t msg_blocks, int first,
+                         uint32_t* flag, cudaStream_t st, bool* handled);
 int launch_quantize_deq(const void* x, int dtype, int64_t n, int bits, int64_t block, uint8_t* codes, void* absmax,
                         void* out, uint32_t* flag, cudaStream_t st, bool* handled);
 int launch_gather_dequant(const void* const* codes, const void* const* absmax, int absmax_dtype, int n_src,

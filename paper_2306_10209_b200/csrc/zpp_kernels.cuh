@@ -902,6 +902,27 @@ __device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, uint32_t 
                : "memory");
 }
 
+// TMA bulk stores (shared -> global, local or a peer's NVLink-mapped memory)
+__device__ __forceinline__ void bulk_s2g(void* gmem, const void* smem, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gmem),
+               "r"((uint32_t)__cvta_generic_to_shared(smem)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait() {
+  asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+// order this thread's generic-proxy shared-memory writes before later
+// async-proxy (bulk copy) reads of them
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 template <int BITS, typename O, int STAGES, int TILE_U>
 __global__ void __launch_bounds__(256)
 dequant16_tma_kernel(SrcTable src, int n_src, int rot, int64_t shard_len, int64_t B, O* __restrict__ out,
@@ -1544,10 +1565,14 @@ __device__ __forceinline__ double div_q_f32(float m) {
 // either the requantized codes (inactive lanes write the zero padding of a
 // partial last block, zs/quantizer.py:215-217) or, when hop 2 is a self-send
 // (FO != void), K3's fold of that one source rounded once to FO.
+// fo_tbl (FO = float, OBITS = 4): the warp's 16-float shared table of the
+// final values, fo_tbl[c + 8] = RN32(RN64(+0.0 + RN64(c * s2))), so a code
+// costs one IMAD + one LDS.32 instead of DSUB + DMUL + F2F (same values).
 template <int OBITS, typename FO>
 __device__ __forceinline__ void drq_epilogue(const double (&acc)[16], int64_t b, int tl, int64_t e0, bool active,
                                              int64_t u, uint8_t* __restrict__ codes, double* __restrict__ absmax,
-                                             uint32_t* __restrict__ flag, FO* __restrict__ final_out) {
+                                             uint32_t* __restrict__ flag, FO* __restrict__ final_out,
+                                             float* fo_tbl = nullptr) {
   constexpr int QMAX = Codes<OBITS>::kQmax;
   double mx = 0.0;
 #pragma unroll
@@ -1579,6 +1604,23 @@ __device__ __forceinline__ void drq_epilogue(const double (&acc)[16], int64_t b,
       *reinterpret_cast<uint4*>(dst) = make_uint4(a.x, a.y, c.x, c.y);
     } else {
       *reinterpret_cast<uint2*>(dst) = make_uint2(pack8_int4(q0), pack8_int4(q1));
+    }
+  } else if (OBITS == 4 && sizeof(FO) == 4 && fo_tbl != nullptr) {
+    const double s2 = scale_of<OBITS>(mx);
+    __syncwarp();  // the previous block's lookups are done
+    if (tl < 16) fo_tbl[tl] = __double2float_rn(__dadd_rn(0.0, __dmul_rn((double)(tl - 8), s2)));
+    __syncwarp();
+    if (active) {
+      const uint32_t base = (uint32_t)__cvta_generic_to_shared(fo_tbl) + 32;  // entry of code 0
+      float v[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const uint32_t a = base + (uint32_t)(__double2loint(r[i]) * 4);
+        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v[i]) : "r"(a) : "memory");
+      }
+      float* dst = reinterpret_cast<float*>(final_out) + e0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) reinterpret_cast<float4*>(dst)[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
     }
   } else if (active) {
     // hop 2 to itself: K3's fold of one source, RN(+0.0 + RN(code*s2)) = RN(code*s2)
@@ -1646,6 +1688,93 @@ drq_fast_kernel(SrcTable src, int64_t n, int lg1, int64_t n_blocks_out, uint8_t*
     drq_epilogue<OBITS, FO>(acc, b, tl, e0, active, u, codes, absmax, flag, final_out);
   }
   if (bad) raise_flag(flag, FLAG_BADCODE);
+}
+
+// ---------------------------------------------------------------------------
+// K1 with the hop-1 all-to-all fused in (push).  The qgZ send buffer [j][c][e]
+// is message j = send blocks [j*mb, (j+1)*mb), destined for
+// local peer j; instead of writing it to this rank's HBM for the peers to
+// pull, each CTA quantizes a tile of TILE consecutive send blocks into shared
+// memory (two alternating staging buffers) and one thread streams the tile's
+// codes and absmax straight into the receiving peers' buffers with TMA bulk
+// stores over NVLink, slot `loc` of peer j's [src_loc][c][e] receive region
+// (zs/collectives.py:519-523: the receiver folds its X messages in ascending
+// source order).  The quantize arithmetic is quant_compute's, unchanged; only
+// the destination differs.  The NVLink transfer thus overlaps the (issue-
+// bound) quantization instead of following it, and K2 reads local HBM.
+constexpr int kMaxPush = 8;
+template <int LANES, int EPL, int BITS>
+struct PushTile {  // a warp tile carries about 2 KB of codes
+  static constexpr int kBB = LANES * EPL * BITS / 8;
+  static constexpr int R = (2048 / kBB) / (32 / LANES) > 1 ? (2048 / kBB) / (32 / LANES) : 1;
+  static constexpr int WT = (32 / LANES) * R;
+};
+struct PushDst {
+  uint8_t* codes[kMaxPush];  // peer j's receive slot for this rank's message (codes)
+  uint8_t* absmax[kMaxPush]; // ... and its fp32 absmax
+  FastDiv mb;                // send blocks per message
+};
+
+template <typename T, int BITS, int LANES, int EPL>
+__global__ void __launch_bounds__(256)
+quantize_push_kernel(const T* __restrict__ x, SwizzleAddr addr, int n_msg, int first, PushDst dst,
+                     uint32_t* __restrict__ flag) {
+  if (comm_aborted(flag)) return;
+  constexpr int TPW = 32 / LANES;
+  constexpr int BB = LANES * EPL * BITS / 8;     // code bytes per block
+  constexpr int R = PushTile<LANES, EPL, BITS>::R;   // team rounds per warp tile
+  constexpr int WT = TPW * R;                    // send blocks per warp tile (~2 KB of codes)
+  static_assert(BB % 16 == 0, "bulk copies move 16-byte multiples");
+  // per-warp staging, two alternating buffers: warps never wait for each other
+  __shared__ __align__(128) uint8_t st_codes[8][2][WT * BB];
+  __shared__ __align__(16) float st_abs[8][2][WT];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int tl = lane % LANES, team = lane / LANES;
+  // Warp tiles never straddle a message, and consecutive tiles go to
+  // different peers (message (first + v) mod n_msg for virtual tile v), so at
+  // any moment the grid's stores are spread over every peer's NVLink ingress
+  // instead of all ranks pushing message 0 to the same GPU first.
+  const int64_t mbs = dst.mb.d;
+  const int64_t tpm = (mbs + WT - 1) / WT;  // warp tiles per message
+  const int64_t tiles = tpm * n_msg;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  int it = 0;
+  for (int64_t v = gw; v < tiles; v += nw, ++it) {
+    const int buf = it & 1;
+    if (it >= 2) {
+      if (lane == 0) bulk_wait_read<1>();  // the stores issued from this buffer two tiles ago have read it
+      __syncwarp();
+    }
+    int j = (int)(v % n_msg) + first;
+    if (j >= n_msg) j -= n_msg;
+    const int64_t off0 = (v / n_msg) * WT;  // first block of the tile inside message j
+    const int nb = (int)min((int64_t)WT, mbs - off0);
+#pragma unroll 1
+    for (int r = 0; r < R; ++r) {
+      const int bl = r * TPW + team;
+      TeamIn<T, EPL> in;
+      quant_load<T, LANES, EPL, SwizzleAddr>(x, addr, (int64_t)j * mbs + off0 + bl, bl < nb, tl, in);
+      quant_compute<T, BITS, LANES, EPL, false>(x, in, bl, bl < nb, tl, st_codes[wid][buf], st_abs[wid][buf], flag,
+                                                nullptr);
+    }
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      bulk_s2g(dst.codes[j] + off0 * BB, st_codes[wid][buf], (uint32_t)(nb * BB));
+      float* da = reinterpret_cast<float*>(dst.absmax[j]) + off0;
+      if ((reinterpret_cast<uintptr_t>(da) & 15) == 0 && nb % 4 == 0) {
+        bulk_s2g(da, st_abs[wid][buf], (uint32_t)(nb * 4));
+      } else {
+        for (int i = 0; i < nb; ++i) da[i] = st_abs[wid][buf][i];
+      }
+      bulk_commit();
+    }
+  }
+  if (lane == 0) {
+    bulk_wait<0>();           // every store performed before the grid completes ...
+    __threadfence_system();   // ... and ordered before the group barrier's release that follows
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1724,12 +1853,13 @@ __device__ __forceinline__ void fold16_tbl4(const uint2& w, uint32_t slot, doubl
 // multiples of 512 (one scale per warp and source).  Every lane loads the
 // block absmax even past the end of a partial last block, so the table inputs
 // are warp-uniform.
-template <int OBITS, int NSRC, typename FO = void>
+template <int OBITS, int NSRC, typename FO = void, int NT = NSRC>
 __global__ void __launch_bounds__(256)
 drq_tbl_kernel(SrcTable src, int64_t n, int lg1, int64_t n_blocks_out, uint8_t* __restrict__ codes,
                double* __restrict__ absmax, uint32_t* __restrict__ flag, FO* __restrict__ final_out = nullptr) {
   if (comm_aborted(flag)) return;
-  __shared__ __align__(256) double tbl_all[8][NSRC * kTblSlotDoubles];
+  __shared__ __align__(256) double tbl_all[8][NT * kTblSlotDoubles];
+  __shared__ __align__(64) float fo_all[8][16];
   const int tl = threadIdx.x & 31;
   double* tbl = tbl_all[threadIdx.x >> 5];
   const uint32_t slot0 = (uint32_t)__cvta_generic_to_shared(tbl);
@@ -1759,13 +1889,22 @@ drq_tbl_kernel(SrcTable src, int64_t n, int lg1, int64_t n_blocks_out, uint8_t* 
     }
     load(b + nwarp, wn, mn);
     __syncwarp();  // the previous block's lookups are done before the tables change
-    tbl4_build<NSRC>(tbl, m, tl);
+    {
+      float mt[NT];
+#pragma unroll
+      for (int j = 0; j < NT; ++j) mt[j] = m[j];
+      tbl4_build<NT>(tbl, mt, tl);
+    }
     __syncwarp();
     double acc[16];
     fold16_tbl4<true>(w[0], slot0, acc, bad);
 #pragma unroll
-    for (int j = 1; j < NSRC; ++j) fold16_tbl4<false>(w[j], slot0 + j * 256, acc, bad);
-    drq_epilogue<OBITS, FO>(acc, b, tl, e0, active, u, codes, absmax, flag, final_out);
+    for (int j = 1; j < NSRC; ++j) {
+      // sources past NT (development split): the plain product path
+      if (j < NT) fold16_tbl4<false>(w[j], slot0 + j * 256, acc, bad);
+      else fold16<4, true>(w[j], div_q_f32<7>(m[j]), acc, bad);
+    }
+    drq_epilogue<OBITS, FO>(acc, b, tl, e0, active, u, codes, absmax, flag, final_out, fo_all[threadIdx.x >> 5]);
   }
   if (bad) raise_flag(flag, FLAG_BADCODE);
 }
@@ -1775,31 +1914,32 @@ drq_tbl_kernel(SrcTable src, int64_t n, int lg1, int64_t n_blocks_out, uint8_t* 
 // lane = 16 contiguous elements, grid-stride, next unit's codes and absmax
 // loaded before this unit is folded (the sources are peers' HBM).  The first
 // source assigns (see fold16).  Same arithmetic as dr_unit.
-template <int BITS, int NSRC, typename A, typename O>
+template <int BITS, int NSRC, typename A, typename O, bool TBL = false>
 __global__ void __launch_bounds__(256)
 dr_fast_kernel(SrcTable src, int64_t n, int lg, O* __restrict__ out, double post_scale, uint32_t* __restrict__ flag) {
   if (comm_aborted(flag)) return;
+  static_assert(!TBL || BITS == 4, "product tables are for INT4 sources");
   using V = typename Vec16<BITS>::T;
+  // TBL (INT4, blocks of >= 512 elements): a warp's 32 units share one block
+  // per source, whose absmax every lane loads (warp-uniform table inputs)
+  __shared__ __align__(256) double tbl_all[TBL ? 8 : 1][TBL ? NSRC * kTblSlotDoubles : 1];
+  const uint32_t slot0 = (uint32_t)__cvta_generic_to_shared(&tbl_all[TBL ? (threadIdx.x >> 5) : 0][0]);
   const int64_t units = n / 16;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   bool bad = false;
   V w[NSRC], wn[NSRC];
   A m[NSRC], mn[NSRC];
   auto load = [&](int64_t u, V (&wv)[NSRC], A (&mv)[NSRC]) {
+    const int64_t ua = TBL ? (u & ~int64_t(31)) : u;
 #pragma unroll
     for (int j = 0; j < NSRC; ++j) {
-      if (u < units) {
-        wv[j] = __ldg(reinterpret_cast<const V*>(src.codes[j]) + u);
-        mv[j] = __ldg(reinterpret_cast<const A*>(src.absmax[j]) + ((u * 16) >> lg));
-      } else {
-        wv[j] = V{};
-        mv[j] = A(0);
-      }
+      wv[j] = u < units ? __ldg(reinterpret_cast<const V*>(src.codes[j]) + u) : V{};
+      mv[j] = ua < units ? __ldg(reinterpret_cast<const A*>(src.absmax[j]) + ((ua * 16) >> lg)) : A(0);
     }
   };
   int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   load(u, wn, mn);
-  for (; u < units; u += stride) {
+  for (; (TBL ? (u & ~int64_t(31)) : u) < units; u += stride) {
 #pragma unroll
     for (int j = 0; j < NSRC; ++j) {
       w[j] = wn[j];
@@ -1807,9 +1947,22 @@ dr_fast_kernel(SrcTable src, int64_t n, int lg, O* __restrict__ out, double post
     }
     load(u + stride, wn, mn);
     double acc[16];
-    fold16<BITS, true, true>(w[0], scale_of<BITS>((double)m[0]), acc, bad);
+    if constexpr (TBL) {
+      double md[NSRC];
 #pragma unroll
-    for (int j = 1; j < NSRC; ++j) fold16<BITS, true>(w[j], scale_of<BITS>((double)m[j]), acc, bad);
+      for (int j = 0; j < NSRC; ++j) md[j] = (double)m[j];
+      __syncwarp();
+      tbl4_build<NSRC>(&tbl_all[threadIdx.x >> 5][0], md, threadIdx.x & 31);
+      __syncwarp();
+      if (u >= units) continue;
+      fold16_tbl4<true>(w[0], slot0, acc, bad);
+#pragma unroll
+      for (int j = 1; j < NSRC; ++j) fold16_tbl4<false>(w[j], slot0 + j * 256, acc, bad);
+    } else {
+      fold16<BITS, true, true>(w[0], scale_of<BITS>((double)m[0]), acc, bad);
+#pragma unroll
+      for (int j = 1; j < NSRC; ++j) fold16<BITS, true>(w[j], scale_of<BITS>((double)m[j]), acc, bad);
+    }
     if (post_scale != 1.0) {
 #pragma unroll
       for (int i = 0; i < 16; ++i) acc[i] = __dmul_rn(acc[i], post_scale);
@@ -1885,17 +2038,22 @@ __device__ __forceinline__ double tma_absmax(const SrcTable& src, int j, const u
 
 // K2 (hop-1 fold + requant into 512-element blocks, or the final partition
 // when hop 2 is a self-send): fp32 absmax sources, warp = output block.
-template <int IBITS, int OBITS, int NSRC, typename FO, int STAGES>
+template <int IBITS, int OBITS, int NSRC, typename FO, int STAGES, bool TBL = false>
 __global__ void __launch_bounds__(256)
 drq_tma_kernel(SrcTable src, int64_t n, TmaTile tt, uint8_t* __restrict__ codes, double* __restrict__ absmax,
                uint32_t* __restrict__ flag, FO* __restrict__ final_out) {
   if (comm_aborted(flag)) return;
+  static_assert(!TBL || IBITS == 4, "product tables are for INT4 sources");
   using V = typename Vec16<IBITS>::T;
   constexpr int UB = 2 * IBITS;
-  constexpr int QMAX = Codes<OBITS>::kQmax;
   extern __shared__ __align__(128) uint8_t dsm[];
+  // TBL (INT4 sources, input blocks of >= 512 elements): one product table per
+  // (warp, source), see tbl4_build
+  __shared__ __align__(256) double tbl_all[TBL ? 8 : 1][TBL ? NSRC * kTblSlotDoubles : 1];
+  __shared__ __align__(64) float fo_all[8][16];
   uint64_t* full = reinterpret_cast<uint64_t*>(dsm + (size_t)STAGES * tt.stage_bytes);
   const int tid = threadIdx.x, tl = tid & 31, wid = tid >> 5;
+  const uint32_t slot0 = (uint32_t)__cvta_generic_to_shared(&tbl_all[TBL ? wid : 0][0]);
   const int64_t units = n / 16;
   const int64_t tiles = (units + tt.tu - 1) / tt.tu;
   const int64_t G = gridDim.x;
@@ -1931,59 +2089,40 @@ drq_tma_kernel(SrcTable src, int64_t n, TmaTile tt, uint8_t* __restrict__ codes,
       const bool active = unit < units;
       if (u0 + ob * 32 >= units) break;  // warp-uniform: block entirely past the end
       double acc[16];
+      if constexpr (TBL) {
+        // the warp's 512 elements share one input block per source
+        const int64_t bw = ((u0 + ob * 32) * 16) >> tt.lg;
+        float m[NSRC];
 #pragma unroll
-      for (int j = 0; j < NSRC; ++j) {
-        const uint8_t* sl = stage + j * (tt.code_slot + tt.abs_slot);
-        V w = active ? *reinterpret_cast<const V*>(sl + lu * UB) : V{};
-        const double m = active ? tma_absmax<float>(src, j, sl + tt.code_slot, b_first, (unit * 16) >> tt.lg) : 0.0;
-        const double sc = div_q_f32<Codes<IBITS>::kQmax>((float)m);
-        if (j == 0) fold16<IBITS, true, true>(w, sc, acc, bad);
-        else fold16<IBITS, true>(w, sc, acc, bad);
-      }
-      double mx = 0.0;
+        for (int j = 0; j < NSRC; ++j)
+          m[j] = (float)tma_absmax<float>(src, j, stage + j * (tt.code_slot + tt.abs_slot) + tt.code_slot, b_first, bw);
+        __syncwarp();  // the previous block's lookups are done before the tables change
+        tbl4_build<NSRC>(&tbl_all[wid][0], m, tl);
+        __syncwarp();
 #pragma unroll
-      for (int i = 0; i < 16; ++i) mx = dmax_nn(mx, fabs(acc[i]));
-#pragma unroll
-      for (int off = 16; off >= 1; off >>= 1) mx = dmax_nn(mx, __shfl_xor_sync(0xffffffffu, mx, off));
-      const int64_t bo = (u0 + ob * 32) / 32;  // output block index
-      if (tl == 0) {
-        absmax[bo] = mx;
-        if (!(mx <= DBL_MAX)) raise_flag(flag, FLAG_NONFINITE);
-      }
-      const double inv = mx > 0.0 ? __ddiv_rn((double)QMAX, mx) : 0.0;
-      double r[16];
-#pragma unroll
-      for (int i = 0; i < 16; ++i) r[i] = __dadd_rn(__dmul_rn(acc[i], inv), kMagic52);
-      if constexpr (std::is_void<FO>::value) {
-        uint32_t q0[8], q1[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          q0[i] = (uint32_t)__double2loint(r[i]);
-          q1[i] = (uint32_t)__double2loint(r[8 + i]);
+        for (int j = 0; j < NSRC; ++j) {
+          const uint8_t* sl = stage + j * (tt.code_slot + tt.abs_slot);
+          const uint2 w = active ? *reinterpret_cast<const uint2*>(sl + lu * UB) : make_uint2(0, 0);
+          if (j == 0) fold16_tbl4<true>(w, slot0, acc, bad);
+          else fold16_tbl4<false>(w, slot0 + j * 256, acc, bad);
         }
-        uint8_t* dst = codes + unit * 2 * OBITS;  // inactive lanes: zero padding
-        if constexpr (OBITS == 8) {
-          const uint2 a = pack8_int8(q0), c = pack8_int8(q1);
-          *reinterpret_cast<uint4*>(dst) = make_uint4(a.x, a.y, c.x, c.y);
-        } else {
-          *reinterpret_cast<uint2*>(dst) = make_uint2(pack8_int4(q0), pack8_int4(q1));
-        }
-      } else if (active) {
-        const double s2 = scale_of<OBITS>(mx);
-        double v[16];
+      } else {
 #pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] = __dmul_rn(__dsub_rn(r[i], kMagic52), s2);
-        FO* dst = final_out + unit * 16;
-        if constexpr (sizeof(FO) == 4) {
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-            reinterpret_cast<float4*>(dst)[i] = make_float4(from_f64<float>(v[4 * i]), from_f64<float>(v[4 * i + 1]),
-                                                            from_f64<float>(v[4 * i + 2]), from_f64<float>(v[4 * i + 3]));
-        } else {
-#pragma unroll
-          for (int i = 0; i < 8; ++i) reinterpret_cast<double2*>(dst)[i] = make_double2(v[2 * i], v[2 * i + 1]);
+        for (int j = 0; j < NSRC; ++j) {
+          const uint8_t* sl = stage + j * (tt.code_slot + tt.abs_slot);
+          V w = active ? *reinterpret_cast<const V*>(sl + lu * UB) : V{};
+          const double m = active ? tma_absmax<float>(src, j, sl + tt.code_slot, b_first, (unit * 16) >> tt.lg) : 0.0;
+          const double sc = div_q_f32<Codes<IBITS>::kQmax>((float)m);
+          if (j == 0) fold16<IBITS, true, true>(w, sc, acc, bad);
+          else fold16<IBITS, true>(w, sc, acc, bad);
         }
       }
+      if (!active) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) acc[i] = 0.0;  // zero padding of a partial last block
+      }
+      drq_epilogue<OBITS, FO>(acc, (u0 + ob * 32) / 32, tl, unit * 16, active, unit, codes, absmax, flag, final_out,
+                              TBL ? fo_all[wid] : nullptr);
     }
     __syncthreads();  // every thread is done with this slot before it is refilled
   }
@@ -1991,15 +2130,19 @@ drq_tma_kernel(SrcTable src, int64_t n, TmaTile tt, uint8_t* __restrict__ codes,
 }
 
 // K3 (hop-2 fold into the rank's partition): f64 absmax sources from K2.
-template <int BITS, int NSRC, typename O, int STAGES>
+template <int BITS, int NSRC, typename O, int STAGES, bool TBL = false>
 __global__ void __launch_bounds__(256)
 dr_tma_kernel(SrcTable src, int64_t n, TmaTile tt, O* __restrict__ out, uint32_t* __restrict__ flag) {
   if (comm_aborted(flag)) return;
+  static_assert(!TBL || BITS == 4, "product tables are for INT4 sources");
   using V = typename Vec16<BITS>::T;
   constexpr int UB = 2 * BITS;
   extern __shared__ __align__(128) uint8_t dsm[];
+  __shared__ __align__(256) double tbl_all[TBL ? 8 : 1][TBL ? NSRC * kTblSlotDoubles : 1];
   uint64_t* full = reinterpret_cast<uint64_t*>(dsm + (size_t)STAGES * tt.stage_bytes);
   const int tid = threadIdx.x;
+  const int wid = tid >> 5;
+  const uint32_t slot0 = (uint32_t)__cvta_generic_to_shared(&tbl_all[TBL ? wid : 0][0]);
   const int64_t units = n / 16;
   const int64_t tiles = (units + tt.tu - 1) / tt.tu;
   const int64_t G = gridDim.x;
@@ -2031,15 +2174,36 @@ dr_tma_kernel(SrcTable src, int64_t n, TmaTile tt, O* __restrict__ out, uint32_t
     const int64_t b_first = (u0 * 16) >> tt.lg;
     for (int lu = tid; lu < tt.tu; lu += 256) {
       const int64_t unit = u0 + lu;
-      if (unit >= units) break;
       double acc[16];
+      if constexpr (TBL) {
+        // warp = 32 units = 512 elements inside one block of every source
+        const int64_t uw = u0 + (lu & ~31);
+        if (uw >= units) break;  // warp-uniform
+        const int64_t bw = (uw * 16) >> tt.lg;
+        double m[NSRC];
 #pragma unroll
-      for (int j = 0; j < NSRC; ++j) {
-        const uint8_t* sl = stage + j * (tt.code_slot + tt.abs_slot);
-        const V w = *reinterpret_cast<const V*>(sl + lu * UB);
-        const double sc = scale_of<BITS>(tma_absmax<double>(src, j, sl + tt.code_slot, b_first, (unit * 16) >> tt.lg));
-        if (j == 0) fold16<BITS, true, true>(w, sc, acc, bad);
-        else fold16<BITS, true>(w, sc, acc, bad);
+        for (int j = 0; j < NSRC; ++j)
+          m[j] = tma_absmax<double>(src, j, stage + j * (tt.code_slot + tt.abs_slot) + tt.code_slot, b_first, bw);
+        __syncwarp();
+        tbl4_build<NSRC>(&tbl_all[wid][0], m, tid & 31);
+        __syncwarp();
+        if (unit >= units) continue;  // past the end (the warp's last loop trip)
+#pragma unroll
+        for (int j = 0; j < NSRC; ++j) {
+          const uint2 w = *reinterpret_cast<const uint2*>(stage + j * (tt.code_slot + tt.abs_slot) + lu * UB);
+          if (j == 0) fold16_tbl4<true>(w, slot0, acc, bad);
+          else fold16_tbl4<false>(w, slot0 + j * 256, acc, bad);
+        }
+      } else {
+        if (unit >= units) break;
+#pragma unroll
+        for (int j = 0; j < NSRC; ++j) {
+          const uint8_t* sl = stage + j * (tt.code_slot + tt.abs_slot);
+          const V w = *reinterpret_cast<const V*>(sl + lu * UB);
+          const double sc = scale_of<BITS>(tma_absmax<double>(src, j, sl + tt.code_slot, b_first, (unit * 16) >> tt.lg));
+          if (j == 0) fold16<BITS, true, true>(w, sc, acc, bad);
+          else fold16<BITS, true>(w, sc, acc, bad);
+        }
       }
       O* dst = out + unit * 16;
       if constexpr (sizeof(O) == 4) {

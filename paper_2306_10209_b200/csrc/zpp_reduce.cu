@@ -36,10 +36,14 @@ static bool codes_aligned(const SrcTable& t, int n_src, int bits) {
 // K3
 
 // K3 fixed fan-in fast path: 2/4/8 sources, power-of-two block, fp32/f64 out
+bool tbl_off();
+
 template <int BITS, int NS, typename A, typename O>
 static int run_reduce_fast(const SrcTable& t, int64_t n, int lg, void* out, double post_scale, uint32_t* flag,
                            cudaStream_t st) {
-  auto k = dr_fast_kernel<BITS, NS, A, O>;
+  // INT4 sources with one scale per warp tile: product tables
+  auto k = (BITS == 4 && lg >= 9 && !tbl_off()) ? dr_fast_kernel<BITS, NS, A, O, BITS == 4>
+                                                : dr_fast_kernel<BITS, NS, A, O, false>;
   const int grid = grid_for(k, 256, ceil_div(n / 16, 256));
   k<<<grid, 256, 0, st>>>(t, n, lg, reinterpret_cast<O*>(out), post_scale, flag);
   return check_cuda(cudaGetLastError(), "dr_fast_kernel launch");
@@ -115,6 +119,15 @@ bool tbl_off() {
   return off;
 }
 
+// ZPP_TBL_SPLIT=2 (development A/B only): 4-source K2 with 2 table sources
+static int tbl_split() {
+  static const int v = [] {
+    const char* e = getenv("ZPP_TBL_SPLIT");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
 template <int IBITS, int OBITS, typename FO>
 static int run_drq_fast(const SrcTable& t, int n_src, int64_t n, int64_t in_block, int64_t nbo, uint8_t* codes,
                         double* absmax, FO* final_out, uint32_t* flag, cudaStream_t st) {
@@ -124,7 +137,8 @@ static int run_drq_fast(const SrcTable& t, int n_src, int64_t n, int64_t in_bloc
 #define ZPP_FAST(NS)                                                                            \
   {                                                                                             \
     if (tbl) {                                                                                  \
-      auto k = drq_tbl_kernel<OBITS, NS, FO>;                                                   \
+      auto k = tbl_split() == 2 && NS == 4 ? drq_tbl_kernel<OBITS, NS, FO, (NS == 4 ? 2 : NS)>   \
+                                             : drq_tbl_kernel<OBITS, NS, FO>;                   \
       const int grid = grid_for(k, 256, ceil_div(nbo, 8));                                      \
       k<<<grid, 256, 0, st>>>(t, n, lg1, nbo, codes, absmax, flag, final_out);                  \
       return check_cuda(cudaGetLastError(), "drq_tbl_kernel launch");                           \
@@ -303,7 +317,9 @@ template <int IB, int OB, int NS, typename FO>
 static int run_drq_tma(const SrcTable& t, int64_t n, int64_t in_block, uint8_t* codes, double* absmax, FO* fo,
                        uint32_t* flag, cudaStream_t st) {
   const TmaTile tt = tma_tile(NS, IB, in_block, sizeof(float));
-  auto k = drq_tma_kernel<IB, OB, NS, FO, kTmaStages>;
+  // INT4 sources with one scale per warp tile: product tables
+  auto k = (IB == 4 && in_block % 512 == 0 && !tbl_off()) ? drq_tma_kernel<IB, OB, NS, FO, kTmaStages, IB == 4>
+                                                          : drq_tma_kernel<IB, OB, NS, FO, kTmaStages, false>;
   size_t smem = 0;
   const int grid = tma_grid(k, tt, ceil_div(n / 16, tt.tu), &smem);
   k<<<grid, 256, smem, st>>>(t, n, tt, codes, absmax, flag, fo);
@@ -356,7 +372,8 @@ int launch_drq_tma(const void* const* codes, const void* const* absmax, int n_sr
 template <int B, int NS, typename O>
 static int run_dr_tma(const SrcTable& t, int64_t n, int64_t block, O* out, uint32_t* flag, cudaStream_t st) {
   const TmaTile tt = tma_tile(NS, B, block, sizeof(double));
-  auto k = dr_tma_kernel<B, NS, O, kTmaStages>;
+  auto k = (B == 4 && block % 512 == 0 && !tbl_off()) ? dr_tma_kernel<B, NS, O, kTmaStages, B == 4>
+                                                      : dr_tma_kernel<B, NS, O, kTmaStages, false>;
   size_t smem = 0;
   const int grid = tma_grid(k, tt, ceil_div(n / 16, tt.tu), &smem);
   k<<<grid, 256, smem, st>>>(t, n, tt, out, flag);

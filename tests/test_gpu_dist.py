@@ -53,6 +53,18 @@ def test_four_gpus_1x4():
     _run(4, 4, 1)
 
 
+@pytest.mark.parametrize("mode", ["push", "pull"])
+def test_qgz_hop1_modes(mode):
+    """Both hop-1 transports (K1 pushing with TMA bulk stores / K2 pulling)
+    on the layouts whose default is the other one: 1xN defaults to pull, 2x2
+    to push (see zpp_qgz_reduce_scatter)."""
+    n = torch.cuda.device_count()
+    _run(2, 2, 2, env={"ZPP_QGZ_MODE": mode})
+    if n >= 4:
+        _run(4, 4, 1, env={"ZPP_QGZ_MODE": mode})
+        _run(4, 2, 2, env={"ZPP_QGZ_MODE": mode})
+
+
 def test_eight_gpus_2x4():
     if torch.cuda.device_count() < 8:
         pytest.skip("needs 8 GPUs")
