@@ -174,6 +174,19 @@ int zpp_qwz_allgather(zpp_comm_t comm, size_t sym_offset, const void* shard, int
                       int64_t block, void* out, int out_dtype, int64_t out_stride, void* sec_out, int64_t sec_lo,
                       int64_t sec_len, void* errflag, void* stream);
 
+/* qwZ all-gather of this layer with the next layer's quantization prefetched
+ * (PAPER.md:611-618): as zpp_qwz_allgather, and when next_shard != NULL, K0 of
+ * next_shard (next_len elements, same dtype and config) is launched on the
+ * communicator's side stream into the next call's half of the symmetric
+ * region, beside this call's NVLink gather.  The next call whose shard is
+ * (next_shard, next_len) waits for that work instead of quantizing.
+ * next_shard must stay unchanged until then.  Prefetch is skipped (the next
+ * call quantizes as usual) when the layout would change or world == 1. */
+int zpp_qwz_allgather_next(zpp_comm_t comm, size_t sym_offset, const void* shard, int dtype, int64_t shard_len,
+                           int bits, int64_t block, void* out, int out_dtype, int64_t out_stride, void* sec_out,
+                           int64_t sec_lo, int64_t sec_len, const void* next_shard, int64_t next_len, void* errflag,
+                           void* stream);
+
 /* hpZ secondary-partition all-gather inside the group over NVLink
  * (zs/collectives.py:202-241 with groups = PartitionSpec.groups()):
  * every rank's secondary shard (sec_len elements of elem_bytes) is held in

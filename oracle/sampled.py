@@ -85,10 +85,13 @@ def qwz_check(out, world: int, shard_len: int, bits: int = 8, block: int = 2048,
 
 
 def qgz_check(out, rank: int, world: int, group: int, n: int, stages: int = 1, inter=(4, 512), intra=None,
-              seed_base: int = 2000, samples: int = 4096, rng_seed: int = 0, slice_len: int | None = None):
+              seed_base: int = 2000, samples: int = 4096, rng_seed: int = 0, slice_len: int | None = None,
+              valid: int | None = None):
     """Check `samples` random output slices (slice_len elements, default the
     larger block) of rank `rank`'s qgZ partition (n // world elements) against
-    the per-slice oracle, bitwise in out's dtype.  Returns (checked, mismatches)."""
+    the per-slice oracle, bitwise in out's dtype.  ``valid``: inputs at bucket
+    positions >= valid are the zero padding of a stream's tail bucket.
+    Returns (checked, mismatches)."""
     intra = intra or inter
     x, y = group, world // group
     part = n // world
@@ -98,6 +101,8 @@ def qgz_check(out, rank: int, world: int, group: int, n: int, stages: int = 1, i
     pick = np.unique(np.concatenate([rng.integers(0, n_sl, size=min(samples, n_sl)), [0, n_sl - 1]]))
     pos = (pick[:, None] * sl + np.arange(sl)[None, :]).reshape(-1)
     src = np.stack([synth.host_at(seed_base + 1000 * q, rank * part + pos, "bf16", "grad") for q in range(world)])
+    if valid is not None:
+        src[:, rank * part + pos >= valid] = 0.0
     want = O.qgz_2hop_slices(src, x, y, inter[0], inter[1], intra[0], intra[1])
     got = _take(out, pos)
     want = want.astype(got.dtype)

@@ -57,6 +57,8 @@ SIGNATURES = {
     "zpp_comm_trace_read": (c_int, [P, P, P, c_int]),
     "zpp_qwz_allgather": (c_int, [P, c_size_t, P, c_int, c_int64, c_int, c_int64, P, c_int, c_int64, P, c_int64,
                                   c_int64, P, P]),
+    "zpp_qwz_allgather_next": (c_int, [P, c_size_t, P, c_int, c_int64, c_int, c_int64, P, c_int, c_int64, P,
+                                       c_int64, c_int64, P, c_int64, P, P]),
     "zpp_hpz_allgather": (c_int, [P, c_size_t, c_int64, c_int, P, P, P]),
     "zpp_qgz_reduce_scatter": (c_int, [P, c_size_t, P, c_int, c_int64, c_int, c_int, c_int, c_int64, c_int,
                                        c_int64, P, c_int, P, P]),

@@ -164,6 +164,14 @@ struct zpp_comm {
   // s run on the caller's stream
   cudaStream_t side = nullptr;
   cudaEvent_t ev_start = nullptr, ev_k1 = nullptr, ev_bar = nullptr;
+  // qwZ cross-layer prefetch (zpp_qwz_allgather_next): K0 of the next shard,
+  // issued on `side` after barrier ev_qbar, completion ev_pf
+  cudaEvent_t ev_pf = nullptr, ev_qbar = nullptr;
+  bool pf_valid = false;
+  const void* pf_ptr = nullptr;
+  int64_t pf_len = 0, pf_block = 0;
+  int pf_dtype = 0, pf_bits = 0;
+  size_t pf_off = 0;
   // stage tracer (zpp_comm_trace): timing events between the launches of the
   // last traced collective, on its stream
   bool trace = false;
@@ -302,18 +310,19 @@ int zpp_comm_reset(zpp_comm_t c) {
   for (int s = 0; s < kScopes; ++s) c->epoch[s] = 0;
   c->qwz_uses = c->qgz_uses = 0;
   c->qwz_region = c->qgz_region = 0;
+  c->pf_valid = false;
   return check_cuda(cudaDeviceSynchronize(), "reset sync");
 }
 
 int zpp_comm_destroy(zpp_comm_t c) {
   if (!c) return ZPP_OK;
   cudaDeviceSynchronize();
-  if (c->side) {
-    cudaEventDestroy(c->ev_start);
-    cudaEventDestroy(c->ev_k1);
-    cudaEventDestroy(c->ev_bar);
-    cudaStreamDestroy(c->side);
-  }
+  if (c->ev_start) cudaEventDestroy(c->ev_start);
+  if (c->ev_k1) cudaEventDestroy(c->ev_k1);
+  if (c->ev_bar) cudaEventDestroy(c->ev_bar);
+  if (c->ev_pf) cudaEventDestroy(c->ev_pf);
+  if (c->ev_qbar) cudaEventDestroy(c->ev_qbar);
+  if (c->side) cudaStreamDestroy(c->side);
   for (int i = 0; i < kTraceMax; ++i)
     if (c->tr_ev[i]) cudaEventDestroy(c->tr_ev[i]);
   for (int r = 0; r < c->world; ++r)
@@ -339,12 +348,39 @@ size_t zpp_qwz_sym_bytes(int64_t shard_len, int bits, int64_t block, int world) 
 int zpp_qwz_allgather(zpp_comm_t c, size_t sym_offset, const void* shard, int dtype, int64_t shard_len, int bits,
                       int64_t block, void* out, int out_dtype, int64_t out_stride, void* sec_out, int64_t sec_lo,
                       int64_t sec_len, void* errflag, void* stream) {
+  return zpp_qwz_allgather_next(c, sym_offset, shard, dtype, shard_len, bits, block, out, out_dtype, out_stride,
+                                sec_out, sec_lo, sec_len, nullptr, 0, errflag, stream);
+}
+
+// Cross-layer prefetch-quantize ("the communication of the
+// current layer and the quantization of the next layer can be launched at the
+// same time on different CUDA streams").  With next_shard, K0 of the next
+// call's shard runs on the side stream into the next call's half, beside this
+// call's NVLink gather (which then leaves kPrefetchSms SMs free for it).
+// Safety: K0(i+1) rewrites the half of call i-1, whose readers (every rank's
+// gather(i-1)) finished before they reached barrier(i); K0(i+1) is ordered
+// after this rank passed barrier(i).  The next call finds the prefetched
+// shard by (pointer, length, config, offset) and waits for it instead of
+// quantizing; any other shard waits for it and is quantized as usual.
+static int qwz_sms_for_prefetch() {
+  static const int v = [] {
+    const char* e = getenv("ZPP_QWZ_PREFETCH_SMS");
+    return e ? atoi(e) : 0;
+  }();
+  return v > 0 ? v : std::max(8, sm_count() / 6);
+}
+
+int zpp_qwz_allgather_next(zpp_comm_t c, size_t sym_offset, const void* shard, int dtype, int64_t shard_len,
+                           int bits, int64_t block, void* out, int out_dtype, int64_t out_stride, void* sec_out,
+                           int64_t sec_lo, int64_t sec_len, const void* next_shard, int64_t next_len, void* errflag,
+                           void* stream) {
   int rc = comm_ok(c);
   if (rc) return rc;
   if ((bits != 4 && bits != 8) || block < 8 || block % 8) return fail(ZPP_ERR_CONFIG, "bad quant config");
   if (shard_len < 0 || (shard_len > 0 && (!shard || !out))) return fail(ZPP_ERR_VALIDATION, "bad arguments");
   if (dtype < 0 || dtype > ZPP_F64 || out_dtype < 0 || out_dtype > ZPP_F64)
     return fail(ZPP_ERR_VALIDATION, "unknown dtype");
+  if (next_shard && next_len <= 0) return fail(ZPP_ERR_VALIDATION, "next_len must be positive");
   const size_t region = qwz_region(shard_len, bits, block, ZPP_F64);
   if (sym_offset + 2 * region > c->sym_bytes) return fail(ZPP_ERR_VALIDATION, "symmetric buffer too small for qwZ");
   if (shard_len == 0) return ZPP_OK;
@@ -352,6 +388,12 @@ int zpp_qwz_allgather(zpp_comm_t c, size_t sym_offset, const void* shard, int dt
   trace_mark(c, TR_BEGIN, reinterpret_cast<cudaStream_t>(stream));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   uint32_t* flag = reinterpret_cast<uint32_t*>(errflag);
+  // a prefetch issued by the previous call for exactly this shard?
+  const bool had_pf = c->pf_valid;
+  const bool use_pf = had_pf && c->pf_ptr == shard && c->pf_len == shard_len && c->pf_dtype == dtype &&
+                      c->pf_bits == bits && c->pf_block == block && c->pf_off == sym_offset;
+  c->pf_valid = false;
+  if (had_pf && (rc = check_cuda(cudaStreamWaitEvent(st, c->ev_pf, 0), "wait prefetch"))) return rc;
   // A different shard length moves the half boundaries, so K0 of this call
   // could overwrite codes peers are still pulling for the previous call (a
   // rank passing that call's barrier only proves peers finished its K0, not
@@ -361,7 +403,8 @@ int zpp_qwz_allgather(zpp_comm_t c, size_t sym_offset, const void* shard, int dt
     if ((rc = barrier(c, 0, kBarrierTimeoutMs, flag, st))) return rc;
   }
   c->qwz_region = region;
-  const size_t base = sym_offset + (c->qwz_uses++ & 1) * region;
+  const uint64_t use = c->qwz_uses++;
+  const size_t base = sym_offset + (use & 1) * region;
   const size_t abs_off = align256((size_t)code_bytes(shard_len, bits, block));
   if (c->world == 1 && sec_out == nullptr && out_dtype == dtype) {
     // 1-GPU world: the gather is the local round trip -- one fused pass
@@ -370,23 +413,58 @@ int zpp_qwz_allgather(zpp_comm_t c, size_t sym_offset, const void* shard, int dt
                              flag, st, &handled);
     if (rc || handled) return rc;
   }
-  AddrSpec a;
-  a.n = shard_len;
-  rc = launch_quantize(shard, dtype, a, shard_len, bits, block, c->local + base,
-                       c->local + base + abs_off, flag, st);
-  if (rc) return rc;
+  if (!use_pf) {
+    AddrSpec a;
+    a.n = shard_len;
+    rc = launch_quantize(shard, dtype, a, shard_len, bits, block, c->local + base, c->local + base + abs_off, flag, st);
+    if (rc) return rc;
+  }
   trace_mark(c, TR_QUANT, st);
   rc = barrier(c, 0, kBarrierTimeoutMs, flag, st);
   if (rc) return rc;
   trace_mark(c, TR_BARRIER, st);
+  // prefetch: K0 of the next shard into the next call's half, on the side
+  // stream, after this rank passed barrier(i); only for an unchanged layout
+  const bool prefetch = next_shard && c->world > 1 && qwz_region(next_len, bits, block, ZPP_F64) == region;
+  if (prefetch) {
+    if (!c->side && (rc = check_cuda(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking), "side stream")))
+      return rc;
+    if (!c->ev_pf && (rc = check_cuda(cudaEventCreateWithFlags(&c->ev_pf, cudaEventDisableTiming), "event")))
+      return rc;
+    if (!c->ev_qbar && (rc = check_cuda(cudaEventCreateWithFlags(&c->ev_qbar, cudaEventDisableTiming), "event")))
+      return rc;
+    if ((rc = check_cuda(cudaEventRecord(c->ev_qbar, st), "record"))) return rc;
+    if ((rc = check_cuda(cudaStreamWaitEvent(c->side, c->ev_qbar, 0), "wait"))) return rc;
+    const size_t nbase = sym_offset + ((use + 1) & 1) * region;
+    const size_t nabs = align256((size_t)code_bytes(next_len, bits, block));
+    AddrSpec a;
+    a.n = next_len;
+    {
+      SmBudget budget(qwz_sms_for_prefetch());
+      rc = launch_quantize(next_shard, dtype, a, next_len, bits, block, c->local + nbase, c->local + nbase + nabs, flag,
+                           c->side);
+    }
+    if (rc) return rc;
+    if ((rc = check_cuda(cudaEventRecord(c->ev_pf, c->side), "record"))) return rc;
+    c->pf_valid = true;
+    c->pf_ptr = next_shard;
+    c->pf_len = next_len;
+    c->pf_dtype = dtype;
+    c->pf_bits = bits;
+    c->pf_block = block;
+    c->pf_off = sym_offset;
+  }
   const void* codes[kMaxRanks];
   const void* absmax[kMaxRanks];
   for (int r = 0; r < c->world; ++r) {
     codes[r] = c->peers[r] + base;
     absmax[r] = c->peers[r] + base + abs_off;
   }
-  rc = launch_gather_dequant(codes, absmax, dtype == ZPP_F64 ? ZPP_F64 : ZPP_F32, c->world, c->rank, shard_len,
-                             bits, block, out, out_dtype, sec_out, sec_lo, sec_len, flag, st, out_stride);
+  {
+    SmBudget budget(prefetch ? sm_count() - qwz_sms_for_prefetch() : 0);
+    rc = launch_gather_dequant(codes, absmax, dtype == ZPP_F64 ? ZPP_F64 : ZPP_F32, c->world, c->rank, shard_len,
+                               bits, block, out, out_dtype, sec_out, sec_lo, sec_len, flag, st, out_stride);
+  }
   trace_mark(c, TR_GATHER, st);
   return rc;
 }
@@ -490,8 +568,8 @@ int zpp_qgz_reduce_scatter(zpp_comm_t c, size_t sym_offset, const void* grad, in
   const int64_t L = l.L;
   const int64_t msg_elems = (int64_t)Y * L;  // one hop-1 message
   const bool pipelined = stages > 1;
-  if (pipelined && !c->side) {
-    rc = check_cuda(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking), "side stream");
+  if (pipelined && !c->ev_start) {
+    if (!c->side) rc = check_cuda(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking), "side stream");
     if (!rc) rc = check_cuda(cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming), "event");
     if (!rc) rc = check_cuda(cudaEventCreateWithFlags(&c->ev_k1, cudaEventDisableTiming), "event");
     if (!rc) rc = check_cuda(cudaEventCreateWithFlags(&c->ev_bar, cudaEventDisableTiming), "event");

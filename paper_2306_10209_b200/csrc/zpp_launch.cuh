@@ -17,13 +17,15 @@ struct SmBudget {
   ~SmBudget() { t_sm_cap = saved; }
 };
 
+// SMs available to the next launch under the current budget
+inline int sm_budget() { return (t_sm_cap > 0 && t_sm_cap < sm_count()) ? t_sm_cap : sm_count(); }
+
 // one resident wave of CTAs (persistent-style grid-stride), capped by work
 template <typename K>
 inline int grid_for(K kernel, int threads, int64_t needed_ctas) {
   int occ = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, 0) != cudaSuccess || occ <= 0) occ = 1;
-  const int sms = (t_sm_cap > 0 && t_sm_cap < sm_count()) ? t_sm_cap : sm_count();
-  int64_t g = (int64_t)sms * occ;
+  int64_t g = (int64_t)sm_budget() * occ;
   if (needed_ctas < g) g = needed_ctas;
   return (int)(g < 1 ? 1 : g);
 }

@@ -104,7 +104,7 @@ class Communicator:
 
     def __init__(self, *, group_size: int | None = None, qwz_shard: int = 0,
                  qwz_cfg: QuantConfig = QuantConfig(bit_width=8, block_size=2048), hpz_sec: int = 0,
-                 hpz_dtype: torch.dtype = torch.float16, qgz_elems: int = 0, qgz_stages: int = 1,
+                 hpz_dtype: torch.dtype = torch.float16, hpz_layers: int = 1, qgz_elems: int = 0, qgz_stages: int = 1,
                  qgz_cfg: QuantConfig = QuantConfig(bit_width=4, block_size=512),
                  qgz_intra_cfg: QuantConfig | None = None):
         self.lib = _lib.load()
@@ -118,13 +118,19 @@ class Communicator:
         self.group_size = group_size
         self.qwz_shard, self.qwz_cfg = qwz_shard, qwz_cfg
         self.hpz_sec, self.hpz_dtype = hpz_sec, hpz_dtype
+        if hpz_layers < 1:
+            raise ValidationError("hpz_layers must be >= 1")
+        self.hpz_layers = hpz_layers
         self.qgz_elems, self.qgz_stages = qgz_elems, qgz_stages
         self.qgz_cfg = qgz_cfg
         self.qgz_intra_cfg = qgz_intra_cfg or qgz_cfg
         hpz_esz = torch.tensor([], dtype=hpz_dtype).element_size()
+        # one secondary slot per layer (the backward gathers of a whole stack
+        # read the secondaries the forward wrote, zs/engine.py:364-370)
+        self._hpz_slot = self.lib.zpp_hpz_sym_bytes(hpz_sec, hpz_esz) if hpz_sec else 0
         self.layout = SymLayout.plan(
             self.lib.zpp_qwz_sym_bytes(qwz_shard, qwz_cfg.bit_width, qwz_cfg.block_size, self.world) if qwz_shard else 0,
-            self.lib.zpp_hpz_sym_bytes(hpz_sec, hpz_esz) if hpz_sec else 0,
+            self._hpz_slot * hpz_layers,
             self.lib.zpp_qgz_sym_bytes(qgz_elems, self.world, qgz_stages, self.qgz_intra_cfg.bit_width,
                                        self.qgz_intra_cfg.block_size, qgz_cfg.bit_width, qgz_cfg.block_size)
             if qgz_elems else 0)
@@ -150,9 +156,12 @@ class Communicator:
         self.flag = torch.zeros(1, dtype=torch.int32, device=device())
         self._broken = False
         if hpz_sec:
-            ptr = self.lib.zpp_comm_sym_ptr(h, self.rank) + self.layout.hpz
-            self._secondary = _wrap_device(ptr, hpz_sec, hpz_dtype)
+            base = self.lib.zpp_comm_sym_ptr(h, self.rank) + self.layout.hpz
+            self._secondaries = [_wrap_device(base + i * self._hpz_slot, hpz_sec, hpz_dtype)
+                                 for i in range(hpz_layers)]
+            self._secondary = self._secondaries[0]
         else:
+            self._secondaries = []
             self._secondary = None
         if initialized:
             dist.barrier()
@@ -161,12 +170,16 @@ class Communicator:
 
     def qwz_allgather(self, shard: torch.Tensor, out: torch.Tensor | None = None,
                       out_dtype: torch.dtype = torch.float16, write_secondary: bool = False,
-                      out_stride: int = 0) -> torch.Tensor:
+                      out_stride: int = 0, next_shard: torch.Tensor | None = None, layer: int = 0) -> torch.Tensor:
         """qwZ: every rank ends with the concatenation (rank order) of every
         rank's dequantize(quantize(shard)) -- zs/collectives.py:244-282.
 
         ``out_stride`` (elements between consecutive ranks' segments, default
-        the shard length) lets a caller gather piece k of every shard in place."""
+        the shard length) lets a caller gather piece k of every shard in place.
+        ``next_shard`` (cross-layer prefetch): the next
+        layer's shard is quantized on a side stream beside this gather; pass it
+        as ``shard`` to the next call and leave it unchanged until then.
+        ``layer`` selects the hpZ secondary slot the write-through fills."""
         self._usable()
         n = int(shard.numel())
         if n > self.qwz_shard:
@@ -189,12 +202,33 @@ class Communicator:
             if sec_hi - sec_lo != self.hpz_sec:
                 raise ValidationError("secondary shard length does not match the communicator's hpz_sec")
             sec_len = sec_hi - sec_lo
-            sec_ptr = self._secondary.data_ptr()
-        _lib.check(self.lib.zpp_qwz_allgather(self.handle, self.layout.qwz, shard.data_ptr(), dtype_code(shard.dtype),
-                                              n, self.qwz_cfg.bit_width, self.qwz_cfg.block_size, out.data_ptr(),
-                                              dtype_code(out.dtype), stride, sec_ptr, sec_lo, sec_len,
-                                              self.flag.data_ptr(), stream_ptr()), "qwz_allgather")
+            sec_ptr = self.secondary_of(layer).data_ptr()
+        nxt, nlen = None, 0
+        if next_shard is not None:
+            nlen = int(next_shard.numel())
+            if nlen > self.qwz_shard or next_shard.dtype != shard.dtype:
+                raise ValidationError("next_shard must fit the communicator and match the shard's dtype")
+            _check_buf(next_shard, "next_shard", nlen)
+            nxt = next_shard.data_ptr()
+        _lib.check(self.lib.zpp_qwz_allgather_next(self.handle, self.layout.qwz, shard.data_ptr(),
+                                                   dtype_code(shard.dtype), n, self.qwz_cfg.bit_width,
+                                                   self.qwz_cfg.block_size, out.data_ptr(), dtype_code(out.dtype),
+                                                   stride, sec_ptr, sec_lo, sec_len, nxt, nlen, self.flag.data_ptr(),
+                                                   stream_ptr()), "qwz_allgather")
         return out
+
+    def qwz_allgather_layers(self, shards, outs=None, write_secondary: bool = False, prefetch: bool = True):
+        """qwZ of a layer sequence (the forward pass of a ZeRO++ step,
+        zs/engine.py:345-360): layer i is gathered while layer i+1 is
+        quantized on the side stream (``prefetch``), and with
+        ``write_secondary`` layer i's hpZ secondary goes to slot i."""
+        outs = outs if outs is not None else [None] * len(shards)
+        res = []
+        for i, sh in enumerate(shards):
+            nxt = shards[i + 1] if prefetch and i + 1 < len(shards) else None
+            res.append(self.qwz_allgather(sh, out=outs[i], write_secondary=write_secondary, next_shard=nxt,
+                                          layer=i if write_secondary else 0))
+        return res
 
     def qwz_allgather_host(self, h_shard: torch.Tensor, h_out: torch.Tensor, chunks: int = 8,
                            d_shard: torch.Tensor | None = None, d_out: torch.Tensor | None = None):
@@ -241,17 +275,27 @@ class Communicator:
             raise ValidationError("communicator has no hpZ secondary region")
         return self._secondary
 
-    def hpz_allgather(self, out: torch.Tensor | None = None) -> torch.Tensor:
+    def secondary_of(self, layer: int) -> torch.Tensor:
+        """This rank's hpZ secondary partition of `layer` (slot in the symmetric workspace)."""
+        if not self._secondaries:
+            raise ValidationError("communicator has no hpZ secondary region")
+        if not 0 <= layer < self.hpz_layers:
+            raise ValidationError(f"layer {layer} outside the communicator's {self.hpz_layers} hpZ slots")
+        return self._secondaries[layer]
+
+    def hpz_allgather(self, out: torch.Tensor | None = None, layer: int = 0) -> torch.Tensor:
         """hpZ: gather the group's secondary shards (member order) over NVLink."""
         self._usable()
         if self._secondary is None:
             raise ValidationError("communicator has no hpZ secondary region")
+        if not 0 <= layer < self.hpz_layers:
+            raise ValidationError(f"layer {layer} outside the communicator's {self.hpz_layers} hpZ slots")
         if out is None:
             out = torch.empty(self.hpz_sec * self.group_size, dtype=self.hpz_dtype, device=device())
         _check_buf(out, "out", self.hpz_sec * self.group_size)
         if out.element_size() != self._secondary.element_size():
             raise ValidationError("hpZ output dtype must match the secondary shard's element size")
-        _lib.check(self.lib.zpp_hpz_allgather(self.handle, self.layout.hpz, self.hpz_sec,
+        _lib.check(self.lib.zpp_hpz_allgather(self.handle, self.layout.hpz + layer * self._hpz_slot, self.hpz_sec,
                                               self._secondary.element_size(), out.data_ptr(), self.flag.data_ptr(),
                                               stream_ptr()), "hpz_allgather")
         return out
@@ -264,6 +308,9 @@ class Communicator:
         n = int(grad.numel())
         if n != self.qgz_elems:
             raise ValidationError(f"gradient has {n} elements, communicator was sized for {self.qgz_elems}")
+        return self._qgz(grad, n, out, out_dtype, reorder)
+
+    def _qgz(self, grad, n, out, out_dtype, reorder):
         _check_buf(grad, "grad", n)
         if out is None:
             out = torch.empty(n // self.world, dtype=out_dtype, device=grad.device)
@@ -274,6 +321,45 @@ class Communicator:
                                                    self.qgz_cfg.bit_width, self.qgz_cfg.block_size, out.data_ptr(),
                                                    dtype_code(out.dtype), self.flag.data_ptr(), stream_ptr()),
                    "qgz_reduce_scatter")
+        return out
+
+    def stream_layout(self, n_total: int) -> tuple[int, int, int, int]:
+        """(full buckets, tail elements, padded tail, output elements per rank)
+        of a gradient stream of n_total elements cut into buckets of
+        ``qgz_elems``; the tail is zero-padded to a multiple of
+        W * S * max(intra block, inter block) (zs/engine.py:465-466)."""
+        bucket = self.qgz_elems
+        full, tail = divmod(n_total, bucket)
+        align = self.world * self.qgz_stages * max(self.qgz_cfg.block_size, self.qgz_intra_cfg.block_size)
+        tail_pad = -(-tail // align) * align
+        return full, tail, tail_pad, (full * bucket + tail_pad) // self.world
+
+    def qgz_reduce_scatter_stream(self, grads: torch.Tensor, out: torch.Tensor | None = None,
+                                  out_dtype: torch.dtype = torch.float32, reorder: bool = True) -> torch.Tensor:
+        """qgZ over a flat gradient stream in buckets of ``qgz_elems`` (the
+        way ZeRO++ reduces a model's gradients, BASELINE configs[3]): bucket b
+        is one qgz_2hop call (zs/collectives.py:464-569) and this rank's
+        output is the concatenation of its partitions of every bucket.  The
+        tail bucket is zero-padded as zs/engine.py:465-466 pads the whole
+        tensor (one device copy into a staging buffer kept by the
+        communicator).  Buckets run back to back on the caller's stream."""
+        self._usable()
+        n_total = int(grads.numel())
+        full, tail, tail_pad, n_out = self.stream_layout(n_total)
+        _check_buf(grads, "grads", n_total)
+        if out is None:
+            out = torch.empty(n_out, dtype=out_dtype, device=grads.device)
+        _check_buf(out, "out", n_out)
+        bucket, w = self.qgz_elems, self.world
+        for b in range(full):
+            self._qgz(grads[b * bucket:(b + 1) * bucket], bucket, out[b * bucket // w:(b + 1) * bucket // w],
+                      out.dtype, reorder)
+        if tail:
+            if getattr(self, "_tail_buf", None) is None or self._tail_buf.numel() != tail_pad \
+                    or self._tail_buf.dtype != grads.dtype:
+                self._tail_buf = torch.zeros(tail_pad, dtype=grads.dtype, device=grads.device)
+            self._tail_buf[:tail].copy_(grads[full * bucket:])
+            self._qgz(self._tail_buf, tail_pad, out[full * bucket // w:], out.dtype, reorder)
         return out
 
     TRACE_STAGES = ("begin", "quantize", "barrier", "gather", "K1", "K2", "K3")

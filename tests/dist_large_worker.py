@@ -41,7 +41,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--group", type=int, default=2)
     ap.add_argument("--samples", type=int, default=4096)
-    ap.add_argument("--cases", default="qwz,qgz,layer")
+    ap.add_argument("--cases", default="qwz,qgz,layer,stream")
     args = ap.parse_args()
     local = int(os.environ["LOCAL_RANK"])
     oversub = os.environ.get("ZPP_OVERSUBSCRIBE") == "1"
@@ -119,6 +119,31 @@ def main():
                                                rng_seed=100 + rank))
         record("layer qgz S=2", *sampled.qgz_check(gout, rank, world, X, layer_p, stages=2, seed_base=5000,
                                                    samples=args.samples))
+        comm.close()
+
+    # ---- a bucketed gradient stream: 3 x 256 MiB buckets + the 7B stream's
+    # 20,678,144-element tail, zero-padded (configs[3], zs/engine.py:465-466) --
+    if "stream" in cases:
+        tail = 20_678_144
+        n_total = 3 * QGZ_BUCKET + tail
+        comm = Communicator(group_size=X, qgz_elems=QGZ_BUCKET, qgz_stages=1,
+                            qgz_cfg=zpp.QuantConfig(bit_width=4, block_size=512))
+        grads = torch.empty(n_total, dtype=torch.bfloat16, device=dev)
+        for b in range(4):
+            lo = b * QGZ_BUCKET
+            synth.device(2000 + 1000 * rank + b, 0, min(QGZ_BUCKET, n_total - lo), torch.bfloat16, "grad",
+                         out=grads[lo:lo + QGZ_BUCKET])
+        full, tl, tail_pad, n_out = comm.stream_layout(n_total)
+        out = comm.qgz_reduce_scatter_stream(grads)
+        out = comm.qgz_reduce_scatter_stream(grads, out=out)
+        comm.check()
+        per = QGZ_BUCKET // world
+        for b in range(full):
+            record(f"stream bucket {b}", *sampled.qgz_check(out[b * per:(b + 1) * per], rank, world, X, QGZ_BUCKET,
+                                                            seed_base=2000 + b, samples=args.samples // 4))
+        record("stream tail", *sampled.qgz_check(out[full * per:], rank, world, X, tail_pad, seed_base=2000 + full,
+                                                 samples=args.samples, valid=tl))
+        del grads, out
         comm.close()
 
     bad = sum(b for _, _, b in report)

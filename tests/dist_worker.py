@@ -151,6 +151,63 @@ def main():
         comm2.check()
         check(f"qgz bucket2 it{it}", same_bits(o2.cpu().numpy(), ref2))
     comm2.close()
+    # ---- cross-layer prefetch-quantize ---------------------
+    n_layers = 4
+    lshard = 2 * 2048 + 512
+    spec_l = zpp.PartitionSpec(total_elems=lshard * world, world=world, group_size=X)
+    llo, lhi = spec_l.secondary_range(rank)
+    lay = [[(np.random.default_rng(500 + 10 * i + r).normal(size=lshard) * 0.02).astype(np.float16)
+            for r in range(world)] for i in range(n_layers)]
+    lwant = [O.all_gather_qwz([s.astype(np.float64) for s in lay[i]], 8, 2048)[0].astype(np.float16)
+             for i in range(n_layers)]
+    comm3 = Communicator(group_size=X, qwz_shard=lshard, hpz_sec=lhi - llo, hpz_layers=n_layers)
+    mine_l = [torch.from_numpy(lay[i][rank]).cuda() for i in range(n_layers)]
+    for prefetch in (True, False, True):
+        outs = comm3.qwz_allgather_layers(mine_l, write_secondary=True, prefetch=prefetch)
+        gs = [comm3.hpz_allgather(layer=i) for i in reversed(range(n_layers))][::-1]  # backward order
+        comm3.check()
+        for i in range(n_layers):
+            check(f"prefetch={prefetch} qwz layer {i}", same_bits(outs[i].cpu().numpy(), lwant[i]))
+            check(f"prefetch={prefetch} hpz layer {i}", same_bits(gs[i].cpu().numpy(), lwant[i]))
+    # a prefetched shard that the next call does not use (it passes another
+    # tensor): the prefetch is waited for and the shard quantized as usual
+    o0 = comm3.qwz_allgather(mine_l[0], next_shard=mine_l[1])
+    o2 = comm3.qwz_allgather(mine_l[2], next_shard=mine_l[3])
+    o3 = comm3.qwz_allgather(mine_l[3])
+    comm3.check()
+    check("prefetch mismatch 0", same_bits(o0.cpu().numpy(), lwant[0]))
+    check("prefetch mismatch 2", same_bits(o2.cpu().numpy(), lwant[2]))
+    check("prefetch used 3", same_bits(o3.cpu().numpy(), lwant[3]))
+    comm3.close()
+
+    # ---- bucketed gradient stream with a zero-padded tail (configs[3]) --------
+    S2 = 1
+    bucket = S2 * world * 2048
+    n_stream = 2 * bucket + 3 * 512 + 77  # two buckets and a ragged tail
+    gs_host = [bf16_bits(np.random.default_rng(700 + r).normal(size=n_stream) * 1e-3) for r in range(world)]
+    comm4 = Communicator(group_size=X, qgz_elems=bucket, qgz_stages=S2,
+                         qgz_cfg=zpp.QuantConfig(bit_width=4, block_size=512))
+    full, tail, tail_pad, n_out = comm4.stream_layout(n_stream)
+    check("stream layout", full == 2 and tail == 3 * 512 + 77 and tail_pad % (world * 512) == 0)
+    want_parts = []
+    for b in range(full + 1):
+        lo_b = b * bucket
+        hi_b = min(lo_b + bucket, n_stream)
+        nb = bucket if b < full else tail_pad
+        srcs = []
+        for r in range(world):
+            v = np.zeros(nb)
+            v[:hi_b - lo_b] = gu.as_f64(gs_host[r][lo_b:hi_b], "bf16")
+            srcs.append(v)
+        want_parts.append(O.qgz_2hop(srcs, X, Y, S2, 4, 512)[rank])
+    want_s = np.concatenate(want_parts)
+    gts = gu.to_torch(gs_host[rank], "bf16")
+    for it in range(2):
+        o_s = comm4.qgz_reduce_scatter_stream(gts, out_dtype=torch.float64)
+        comm4.check()
+        check(f"qgz stream it{it}", o_s.numel() == n_out and same_bits(o_s.cpu().numpy(), want_s))
+    comm4.close()
+
     # ---- process groups for the staged comparators ---------------------------
     mine_pg, cross_pg = make_groups(X)
     check("groups", dist.get_world_size(mine_pg) == X and dist.get_world_size(cross_pg) == Y)
