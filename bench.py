@@ -11,9 +11,13 @@ the whole buffer.
 
 value = whole-job qwZ effective GB/s = N * (2*M fp16 bytes delivered per rank)
 / step time (max over ranks, CUDA events).  Extra keys: the roofline of the
-dominant kernel, the CPU reference timed on this host, an end-to-end number
-through host buffers, clocks during the timed region, the NCCL fp16
-all-gather comparator, and the qgZ 256 MiB bf16 gradient bucket (configs[3]).
+dominant kernel (NVLink 900 GB/s at N > 1), busbw, sampled bitwise parity of
+every leg against the oracle, the CPU reference timed on this host, an
+end-to-end number through host buffers, clocks during the timed region, the
+NCCL comparators, and one leg per other BASELINE config: config-1 16M fp32
+round trip, the qgZ 256 MiB bucket with its roofline, the hpZ group gather,
+the 7B qgZ gradient stream, and the 40-layer GPT-13B ZeRO++ step with and
+without cross-layer prefetch.  ZPP_BENCH_LEGS selects legs.
 """
 
 from __future__ import annotations
@@ -51,7 +55,9 @@ def emit(line: dict) -> None:
 METRIC = "qwZ/qgZ effective GB/s at 1/2/4/8 B200; quant kernel HBM GB/s vs 8 TB/s"
 M_PARAMS = 1_300_004_864           # 1.3e9 rounded up to a multiple of 8 * 2048
 QGZ_BUCKET = 134_217_728           # 256 MiB of bf16 gradients
+NVLINK_NOMINAL_GBS = 900.0         # NVLink 5 per direction per GPU (north_star's roofline)
 NVLINK_PEER_GBS = 770.0            # measured peer copy per direction (B200_PROFILING.md)
+TMA_PULL_GBS = {2: 644.0, 4: 662.0}  # measured TMA bulk-pull ingress ceiling (profiles/p2p_bw_r1_n{2,4}.txt)
 
 
 def peaks():
@@ -195,6 +201,7 @@ def run_ours(args):
     import torch.distributed as dist
 
     import paper_2306_10209_b200 as zpp
+    from oracle import sampled, synth
     from paper_2306_10209_b200 import _lib
     from paper_2306_10209_b200.dist import Communicator, nccl_allgather, nccl_reduce_scatter
 
@@ -214,17 +221,22 @@ def run_ours(args):
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    sections = set(os.environ.get("ZPP_BENCH_LEGS", "qgz,config1,hpz,stream,step").split(","))
     lib = _lib.load()
     dev = torch.device("cuda", local)
+    X = min(world, 4)
     shard_len = M_PARAMS // world
     cfg = zpp.QuantConfig(bit_width=8, block_size=2048)
     qgz_cfg = zpp.QuantConfig(bit_width=4, block_size=512)
-    comm = Communicator(group_size=min(world, 4), qwz_shard=shard_len, qwz_cfg=cfg, qgz_elems=QGZ_BUCKET,
-                        qgz_stages=1, qgz_cfg=qgz_cfg)
-    g = torch.Generator(device=dev).manual_seed(1000 + rank)
-    shard = (torch.randn(shard_len, generator=g, device=dev) * 0.02).half()
+    comm = Communicator(group_size=X, qwz_shard=shard_len, qwz_cfg=cfg, qgz_elems=QGZ_BUCKET, qgz_stages=1,
+                        qgz_cfg=qgz_cfg)
+    # seeded counter-based inputs (oracle/synth.py): any element of any rank's
+    # input can be recomputed on the host for the sampled parity check below
+    shard = synth.device(1000 + rank, 0, shard_len, torch.float16, "weight", device=dev)
     out = torch.empty(M_PARAMS, dtype=torch.float16, device=dev)
     stream = torch.cuda.current_stream()
+    hbm_peak, peak_kind = peaks()
+    parity = {}
 
     def barrier():
         if world > 1:
@@ -237,6 +249,17 @@ def run_ours(args):
         t = torch.tensor([x], dtype=torch.float64, device="cpu" if oversub else dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
+
+    def sum_over_ranks(vals):
+        if world == 1:
+            return list(vals)
+        t = torch.tensor(list(vals), dtype=torch.float64, device="cpu" if oversub else dev)
+        dist.all_reduce(t)
+        return [int(v) for v in t.tolist()]
+
+    def add_parity(name, checked, bad):
+        c, b = sum_over_ranks([checked, bad])
+        parity[name] = {"checked": int(c), "mismatches": int(b)}
 
     def timed(fn, steps, warmup):
         for _ in range(warmup):
@@ -280,14 +303,16 @@ def run_ours(args):
         time.sleep(0.06)
     clk = clocks.stop() if rank == 0 else None
     comm.check()
+    # sampled bitwise parity of the gathered weights after the timed region
+    add_parity("qwz", *sampled.qwz_check(out, world, shard_len, samples=4096, rng_seed=rank))
     # N = 1: one fused quantize->dequantize kernel; N > 1: quantize, barrier, TMA gather
     launches_per_step = 1 if world == 1 else 3
     value = world * 2 * M_PARAMS / t_step / 1e9
+    qbytes = shard_len + shard_len // 2048 * 4
+    busbw_qwz = 2 * M_PARAMS * (world - 1) / world / t_step / 1e9 if world > 1 else None
 
     # ---- per-kernel roofline (CUDA events around each kernel alone) ----------
-    hbm_peak, peak_kind = peaks()
     sym0 = [lib.zpp_comm_sym_ptr(comm.handle, r) for r in range(world)]
-    qbytes = shard_len + shard_len // 2048 * 4
     codes_off, abs_off = comm.layout.qwz, comm.layout.qwz + ((shard_len + 255) // 256 * 256)
     st = stream.cuda_stream
     qcodes = sym0[rank] + codes_off
@@ -325,23 +350,26 @@ def run_ours(args):
     else:
         ingress = (world - 1) * qbytes
         ach = ingress / kg / 1e9
+        nvl = traffic.get(f"nvlink_n{world}", {})
         roof = {"kernel": "dequant16_tma_kernel (gather over NVLink)", "bound": "nvlink", "achieved": ach,
-                "peak": NVLINK_PEER_GBS, "unit": "GB/s", "frac": ach / NVLINK_PEER_GBS,
-                # ncu cannot profile a multi-rank launch; the 1-GPU capture of the same
-                # kernel (4 local sources -> 1.3B fp16) is reported under "hbm" instead
-                "traffic": None,
-                "peak_kind": "measured peer copy, per direction",
+                "peak": NVLINK_NOMINAL_GBS, "unit": "GB/s", "frac": ach / NVLINK_NOMINAL_GBS,
+                # ncu of one rank under real peer traffic (tools/ncu_rank0.sh): NVLink rx
+                # bytes of the gather per launch, at the GPT-13B-layer shape it was captured
+                # at, scaled to this launch's algorithmic ingress
+                "traffic": nvl.get("gather_nvlrx_per_alg_byte", None) and nvl["gather_nvlrx_per_alg_byte"] * ingress,
+                "traffic_source": nvl.get("source"),
+                "peak_kind": "NVLink 5 nominal, per direction (north_star)",
+                "secondary": {"measured_peer_copy_gbs": NVLINK_PEER_GBS, "frac_peer_copy": ach / NVLINK_PEER_GBS,
+                              "measured_tma_pull_gbs": TMA_PULL_GBS.get(world),
+                              "frac_tma_pull": ach / TMA_PULL_GBS[world] if world in TMA_PULL_GBS else None},
                 "alg_bytes_per_launch": ingress, "launch_us": kg * 1e6, "kernels": kern,
                 "hbm": {"achieved": kern["dequant16_kernel (gather)"]["GBps"], "peak": hbm_peak,
-                        "frac": kern["dequant16_kernel (gather)"]["GBps"] / hbm_peak,
-                        "traffic_1gpu_capture": traffic.get("dequant16_tma_kernel (gather over NVLink)"),
-                        "alg_bytes_1gpu_capture": 4 * (M_PARAMS // 4 + M_PARAMS // 4 // 2048 * 4) + 2 * M_PARAMS}}
+                        "frac": kern["dequant16_kernel (gather)"]["GBps"] / hbm_peak}}
 
     # ---- end to end through host buffers ------------------------------------
     h_in = torch.empty(shard_len, dtype=torch.float16, pin_memory=True)
     h_in.copy_(shard.cpu())
     h_out = torch.empty(M_PARAMS, dtype=torch.float16, pin_memory=True)
-
     d_in = torch.empty_like(shard)
 
     def e2e_step():  # host -> device -> fused qwZ -> host, chunk-pipelined over 3 streams
@@ -354,47 +382,46 @@ def run_ours(args):
            "d2h_bytes_per_step": 2 * M_PARAMS, "ms_per_step": t_e2e * 1e3,
            "path": "pinned host shard -> Communicator.qwz_allgather_host (H2D, fused qwZ and D2H overlapped in "
                    "16 chunks) -> pinned host gathered fp16 weights"}
-    del h_out, h_in
+    del h_out, h_in, d_in
 
     # ---- comparators and qgZ ---------------------------------------------------
     extra = {}
     if world > 1 and not oversub:
         t_nccl = timed(lambda: nccl_allgather(shard, out=out), args.steps, 2)
         extra["nccl_fp16_allgather"] = {"value": world * 2 * M_PARAMS / t_nccl / 1e9, "unit": "GB/s",
-                                        "ms_per_step": t_nccl * 1e3}
-    grad = (torch.randn(QGZ_BUCKET, generator=g, device=dev) * 1e-3).bfloat16()
-    part = torch.empty(QGZ_BUCKET // world, dtype=torch.float32, device=dev)
-    t_qgz = timed(lambda: comm.qgz_reduce_scatter(grad, out=part), args.steps, 2)
-    comm.check()
-    X, Y = comm.group_size, world // comm.group_size
-    L = QGZ_BUCKET // world
-    wire = (X - 1) * (Y * L // 2 + Y * L // 512 * 4) + (Y - 1) * (L // 2 + L // 512 * 8)
-    extra["qgz"] = {"workload": "qgZ INT4/512 2-hop reduce-scatter of a 256 MiB bf16 bucket", "groups": f"{Y}x{X}",
-                    "ms_per_bucket": t_qgz * 1e3,
-                    "effective_GBps": world * 2 * QGZ_BUCKET * (world - 1) / world / t_qgz / 1e9 if world > 1 else
-                    2 * QGZ_BUCKET / t_qgz / 1e9,
-                    "wire_bytes_per_gpu": wire}
-    if world > 1 and not oversub:
-        gb = grad.clone()
-        pb = torch.empty(QGZ_BUCKET // world, dtype=torch.bfloat16, device=dev)
-        t_rs = timed(lambda: nccl_reduce_scatter(gb, out=pb), args.steps, 2)
-        extra["nccl_bf16_reduce_scatter"] = {"ms_per_bucket": t_rs * 1e3,
-                                             "effective_GBps": world * 2 * QGZ_BUCKET * (world - 1) / world / t_rs / 1e9}
-
-    extra["hpz"] = hpz_leg(comm_cls=Communicator, world=world, dev=dev, g=g, timed=lambda f: timed(f, args.steps, 2),
-                           oversub=oversub, nccl_allgather=nccl_allgather)
-    extra["zeropp_step_13b_layer"] = step_leg(world=world, dev=dev, g=g, timed=lambda f: timed(f, max(5, args.steps // 2), 2),
-                                              oversub=oversub, comm_cls=Communicator, zpp=zpp,
-                                              nccl_allgather=nccl_allgather, nccl_reduce_scatter=nccl_reduce_scatter)
+                                        "ms_per_step": t_nccl * 1e3,
+                                        "busbw_GBps": 2 * M_PARAMS * (world - 1) / world / t_nccl / 1e9}
+    del out
+    torch.cuda.empty_cache()
+    if "qgz" in sections:
+        extra["qgz"] = qgz_leg(comm=comm, world=world, rank=rank, X=X, dev=dev, timed=timed, steps=args.steps,
+                               hbm_peak=hbm_peak, oversub=oversub, add_parity=add_parity, synth=synth,
+                               sampled=sampled, nccl_reduce_scatter=nccl_reduce_scatter, traffic=traffic)
+    comm.close()
+    torch.cuda.empty_cache()
+    if "config1" in sections:
+        extra["config1_roundtrip_16M_fp32"] = config1_leg(lib=lib, dev=dev, rank=rank, timed_flush=None, steps=args.steps,
+                                                          hbm_peak=hbm_peak, add_parity=add_parity,
+                                                          max_over_ranks=max_over_ranks, barrier=barrier, _lib=_lib)
+    if "hpz" in sections:
+        extra["hpz"] = hpz_leg(comm_cls=Communicator, world=world, dev=dev, timed=lambda f: timed(f, args.steps, 2),
+                               oversub=oversub, nccl_allgather=nccl_allgather, synth=synth, sampled=sampled,
+                               add_parity=add_parity, rank=rank)
+    if "stream" in sections:
+        extra["qgz_stream_7b"] = stream_leg(comm_cls=Communicator, world=world, rank=rank, X=X, dev=dev, timed=timed,
+                                            steps=args.steps, hbm_peak=hbm_peak, synth=synth, sampled=sampled,
+                                            add_parity=add_parity, zpp=zpp)
+    if "step" in sections:
+        extra["zeropp_step_13b"] = step_leg(world=world, rank=rank, dev=dev, timed=timed, steps=args.steps,
+                                            oversub=oversub, comm_cls=Communicator, zpp=zpp, synth=synth,
+                                            sampled=sampled, add_parity=add_parity, nccl_allgather=nccl_allgather,
+                                            nccl_reduce_scatter=nccl_reduce_scatter)
     kq_gbs = kern["quantize_reg_kernel"]["GBps"]
     extra["quant_kernel_hbm"] = {"kernel": "quantize_reg_kernel (K0: fp16 shard -> INT8/2048 codes + absmax)",
                                  "achieved_GBps": kq_gbs, "frac_of_8TBs_nominal": kq_gbs / 8000.0,
                                  "frac_of_measured_peak": kq_gbs / hbm_peak, "shard_elems": shard_len}
-    extra["params_per_s"] = {"qwz": world * M_PARAMS / t_step, "qgz": world * QGZ_BUCKET / t_qgz,
-                             "note": "whole-job parameters (or gradients) delivered per second"}
-    if world > 1:
-        extra["nvlink_nominal"] = {"peak": 900.0, "unit": "GB/s", "qwz_ingress_frac": (world - 1) * qbytes / kg / 1e9 / 900.0,
-                                   "qgz_wire_frac": wire / t_qgz / 1e9 / 900.0}
+    extra["params_per_s"] = {"qwz": world * M_PARAMS / t_step,
+                             "note": "whole-job parameters delivered per second (qgZ: see qgz.params_per_s)"}
 
     line = None
     if rank == 0:
@@ -407,7 +434,8 @@ def run_ours(args):
             "config": {"workload": f"qwZ INT8/2048 fused all-gather of a 1.3B fp16 weight buffer over {world} GPU(s)"
                                    + (" (W=1: quantize->dequantize round trip)" if world == 1 else " (NVLink P2P)"),
                        "M": M_PARAMS, "shard_elems": shard_len, "quant": "int8/2048", "out_dtype": "fp16",
-                       "parallelism": f"zero3-dp{world}", "groups": f"{world // comm.group_size}x{comm.group_size}",
+                       "parallelism": f"zero3-dp{world}", "groups": f"{world // X}x{X}",
+                       "inputs": "seeded counter-based generator (oracle/synth.py), generated on the device",
                        "l2": "inputs and outputs larger than L2 (shard + 2.6 GB fp16 output per step), no flush"}
                       | ({"oversubscribed": "functional check, ranks share GPUs: not a measurement"} if oversub else {}),
             "roofline": roof,
@@ -415,13 +443,19 @@ def run_ours(args):
                              "sample": f"{1 << 25} fp16 elements, numpy oracle port of zs/quantizer.py "
                                        "quantize+dequantize, block-parallel over host threads, median of 3"},
             "e2e": e2e, "clocks": clk, "gpu_launches": launches_per_step * args.steps,
+            "busbw": {"qwz_GBps": busbw_qwz, "qgz_GBps": extra.get("qgz", {}).get("busbw_GBps"),
+                      "definition": "SURVEY 8d collective effective GB/s: 2*M*(W-1)/W / t (fp16/bf16-equivalent "
+                                    "bytes per GPU), NCCL busbw for the same collective; null at W=1"},
+            "parity": parity | {"total_checked": sum(v["checked"] for v in parity.values()),
+                                "total_mismatches": sum(v["mismatches"] for v in parity.values()),
+                                "how": "after the timed regions: sampled outputs (whole 2048-blocks / 512-slices, "
+                                       "summed over ranks) recomputed bitwise by the oracle from the seeded inputs"},
             "qwz": {"ms_per_step": t_step * 1e3,
                     "wire_ingress_bytes_per_gpu": (world - 1) * qbytes,
                     "fp16_allgather_ingress_bytes_per_gpu": (world - 1) * 2 * shard_len},
         }
         line.update(extra)
         emit(line)
-    comm.close()
     if world > 1:
         dist.destroy_process_group()
     return 0
@@ -431,7 +465,126 @@ def _pad(n: int, align: int) -> int:
     return (n + align - 1) // align * align
 
 
-def hpz_leg(*, comm_cls, world, dev, g, timed, oversub, nccl_allgather):
+def qgz_bytes(n, world, X, in_block=512, out_block=512, final_bytes=4):
+    """Per-GPU wire and algorithmic HBM bytes of one INT4 qgZ reduce-scatter of
+    an n-element bf16 bucket: K1 reads bf16 and writes INT4 codes
+    + fp32 absmax; K2 reads X messages of Y*L and writes Y*L INT4 codes + f64
+    absmax (or, with one group, the fp32 partition); K3 reads Y segments of L
+    and writes the fp32 partition."""
+    Y = world // X
+    L = n // world
+    c4 = lambda m, b, a: m // 2 + m // b * a
+    wire = (X - 1) * c4(Y * L, in_block, 4) + (Y - 1) * c4(L, out_block, 8)
+    k1 = 2 * n + c4(n, in_block, 4)
+    if Y == 1:
+        k2 = X * c4(L, in_block, 4) + final_bytes * L
+        k3 = 0
+    else:
+        k2 = X * c4(Y * L, in_block, 4) + c4(Y * L, out_block, 8)
+        k3 = Y * c4(L, out_block, 8) + final_bytes * L
+    return wire, k1 + k2 + k3
+
+
+def qgz_leg(*, comm, world, rank, X, dev, timed, steps, hbm_peak, oversub, add_parity, synth, sampled,
+            nccl_reduce_scatter, traffic):
+    """BASELINE configs[3], one bucket: qgZ INT4/512 2-hop reduce-scatter of a
+    256 MiB bf16 gradient bucket (S = 1), with its roofline
+    t_roof = max(wire / 900 GB/s, HBM / peak)."""
+    import torch
+
+    grad = synth.device(2000 + 1000 * rank, 0, QGZ_BUCKET, torch.bfloat16, "grad", device=dev)
+    part = torch.empty(QGZ_BUCKET // world, dtype=torch.float32, device=dev)
+    t_qgz = timed(lambda: comm.qgz_reduce_scatter(grad, out=part), steps, 3)
+    comm.check()
+    add_parity("qgz", *sampled.qgz_check(part, rank, world, X, QGZ_BUCKET, samples=4096))
+    wire, hbm = qgz_bytes(QGZ_BUCKET, world, X)
+    t_roof = max(wire / (NVLINK_NOMINAL_GBS * 1e9), hbm / (hbm_peak * 1e9))
+    res = {"workload": "qgZ INT4/512 2-hop reduce-scatter of a 256 MiB bf16 bucket, S=1", "groups": f"{world // X}x{X}",
+           "hop1": "K1 pushes (TMA bulk stores)" if world // X > 1 else "K2 pulls (TMA ring)",
+           "ms_per_bucket": t_qgz * 1e3,
+           "effective_GBps": world * 2 * QGZ_BUCKET / t_qgz / 1e9,
+           "busbw_GBps": 2 * QGZ_BUCKET * (world - 1) / world / t_qgz / 1e9 if world > 1 else None,
+           "params_per_s": world * QGZ_BUCKET / t_qgz,
+           "wire_bytes_per_gpu": wire, "hbm_alg_bytes_per_gpu": hbm,
+           "roofline": {"t_roof_us": t_roof * 1e6, "bound": "nvlink" if wire / 900e9 > hbm / (hbm_peak * 1e9) else "hbm",
+                        "frac": t_roof / t_qgz, "nvlink_wire_GBps": wire / t_qgz / 1e9 if wire else None,
+                        "nvlink_frac_of_900": wire / t_qgz / 1e9 / NVLINK_NOMINAL_GBS if wire else None,
+                        "hbm_GBps": hbm / t_qgz / 1e9, "hbm_frac": hbm / t_qgz / 1e9 / hbm_peak,
+                        "note": "t_roof = max(wire/900 GB/s, HBM/peak); the path is bound by neither: the bit-exact "
+                                "f64 fold and the tie-checked quantizer are issue-bound (DESIGN.md, qgZ)"},
+           "bf16_reduce_scatter_wire_bytes_per_gpu": 2 * QGZ_BUCKET * (world - 1) // world}
+    if world > 1 and not oversub:
+        gb = grad.clone()
+        pb = torch.empty(QGZ_BUCKET // world, dtype=torch.bfloat16, device=dev)
+        t_rs = timed(lambda: nccl_reduce_scatter(gb, out=pb), steps, 3)
+        res["nccl_bf16_reduce_scatter"] = {"ms_per_bucket": t_rs * 1e3,
+                                           "busbw_GBps": 2 * QGZ_BUCKET * (world - 1) / world / t_rs / 1e9,
+                                           "speedup_qgz_vs_nccl": t_rs / t_qgz}
+        del gb, pb
+    del grad, part
+    return res
+
+
+def config1_leg(*, lib, dev, rank, timed_flush, steps, hbm_peak, add_parity, max_over_ranks, barrier, _lib):
+    """BASELINE configs[0]: INT8/2048 quantize -> dequantize round trip of a
+    16M-element fp32 tensor (two kernels, fp32 out).  64 MiB fits in L2, so L2
+    is flushed (a 512 MiB write) before every timed round trip."""
+    import torch
+
+    from oracle import synth, zpp_oracle as O
+
+    n = 1 << 24
+    x = synth.device(10 + rank, 0, n, torch.float32, "weight", device=dev)
+    nb = n // 2048
+    codes = torch.empty(n, dtype=torch.uint8, device=dev)
+    absmax = torch.empty(nb, dtype=torch.float32, device=dev)
+    y = torch.empty(n, dtype=torch.float32, device=dev)
+    flag = torch.zeros(1, dtype=torch.int32, device=dev)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    st = torch.cuda.current_stream()
+    sp = st.cuda_stream
+
+    def rt():
+        lib.zpp_quantize(x.data_ptr(), _lib.F32, n, 8, 2048, codes.data_ptr(), absmax.data_ptr(), flag.data_ptr(), sp)
+        lib.zpp_dequantize(codes.data_ptr(), absmax.data_ptr(), _lib.F32, n, 8, 2048, y.data_ptr(), _lib.F32,
+                           flag.data_ptr(), sp)
+
+    for _ in range(3):
+        rt()
+    barrier()
+    evs = []
+    for _ in range(max(steps, 10)):
+        flush.fill_(1)
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(st)
+        rt()
+        e.record(st)
+        evs.append((s, e))
+    torch.cuda.synchronize()
+    t = max_over_ranks(statistics.median(s.elapsed_time(e) for s, e in evs) * 1e-3)
+    if int(flag.item()):
+        raise RuntimeError("config-1 round trip raised a device flag")
+    alg = 2 * (4 * n + n + nb * 4)  # quantize: read fp32 + write codes + absmax; dequantize: the reverse
+    # full-size parity on the host (rank 0's tensor): codes and fp32 output bitwise
+    if rank == 0:
+        xh = synth.host(10, 0, n, "fp32", "weight")
+        c_ref, s_ref, _ = O.quantize(xh, 8, 2048)
+        y_ref = O.dequantize(c_ref, s_ref, n, 8, 2048).astype(np.float32)
+        bad = int(np.count_nonzero(codes.cpu().numpy() != c_ref)) + \
+            int(np.count_nonzero(y.cpu().numpy().view(np.uint32) != y_ref.view(np.uint32)))
+        add_parity("config1", 2 * n, bad)
+    else:
+        add_parity("config1", 0, 0)
+    del x, codes, absmax, y, flush
+    torch.cuda.empty_cache()
+    return {"workload": "INT8/2048 quantize->dequantize of 16,777,216 fp32 (zpp_quantize + zpp_dequantize)",
+            "us_per_roundtrip": t * 1e6, "alg_bytes": alg,
+            "roofline": {"bound": "hbm", "achieved": alg / t / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": alg / t / 1e9 / hbm_peak},
+            "l2": "flushed (512 MiB write) before each timed round trip; median of per-round-trip CUDA events"}
+
+
+def hpz_leg(*, comm_cls, world, dev, timed, oversub, nccl_allgather, synth, sampled, add_parity, rank):
     """BASELINE configs[2]: hpZ gather of one GPT-1.3B layer (12h^2+13h, h=2048)
     inside a group of min(N, 4) consecutive GPUs, vs NCCL's full-box and group
     fp16 all-gathers.  The secondary shard is written through by the qwZ gather
@@ -446,17 +599,21 @@ def hpz_leg(*, comm_cls, world, dev, g, timed, oversub, nccl_allgather):
     layer_p = _pad(layer, world * 2048)
     sec = layer_p // X
     comm = comm_cls(group_size=X, qwz_shard=layer_p // world, hpz_sec=sec)
-    w = (torch.randn(layer_p // world, generator=g, device=dev) * 0.02).half()
+    w = synth.device(3000 + rank, 0, layer_p // world, torch.float16, "weight", device=dev)
     comm.qwz_allgather(w, write_secondary=True)
     comm.check()
     out = torch.empty(layer_p, dtype=torch.float16, device=dev)
     t = timed(lambda: comm.hpz_allgather(out=out))
     comm.check()
+    # every group holds a full replica of the layer split over its X members
+    # (zs/partitioner.py:67-82), so the group gather returns the whole layer
+    add_parity("hpz", *sampled.qwz_check(out, world, layer_p // world, seed_base=3000, samples=2048, rng_seed=rank))
     comm.close()
     ingress = (X - 1) * sec * 2
     res = {"workload": "hpZ fp16 gather of one GPT-1.3B layer inside a group", "layer_params": layer,
            "padded": layer_p, "group_size": X, "ms": t * 1e3, "ingress_bytes_per_gpu": ingress,
-           "ingress_GBps": ingress / t / 1e9, "cross_group_bytes": 0}
+           "ingress_GBps": ingress / t / 1e9, "nvlink_frac_of_900": ingress / t / 1e9 / NVLINK_NOMINAL_GBS,
+           "cross_group_bytes": 0}
     if world > 1 and not oversub:
         full_out = torch.empty(layer_p, dtype=torch.float16, device=dev)
         res["nccl_fullbox_fp16_ag_ms"] = timed(lambda: nccl_allgather(w, out=full_out)) * 1e3
@@ -467,44 +624,114 @@ def hpz_leg(*, comm_cls, world, dev, g, timed, oversub, nccl_allgather):
     return res
 
 
-def step_leg(*, world, dev, g, timed, oversub, comm_cls, zpp, nccl_allgather, nccl_reduce_scatter):
-    """BASELINE configs[4]: the communication of one GPT-13B layer (h=5120) of a
-    ZeRO++ step -- forward qwZ (INT8/2048, writes the hpZ secondary), backward
-    hpZ gather inside the group, gradient qgZ (INT4/512, S=2) -- vs ZeRO-3's
-    fp16 all-gather x2 + bf16 reduce-scatter (NCCL)."""
+def stream_leg(*, comm_cls, world, rank, X, dev, timed, steps, hbm_peak, synth, sampled, add_parity, zpp):
+    """BASELINE configs[3] as written: qgZ INT4/512 over a 7B-parameter bf16
+    gradient stream -- 52 buckets of 256 MiB plus a 20,678,144-element tail
+    zero-padded to W*S*512 (zs/engine.py:465-466) -- back to back through
+    Communicator.qgz_reduce_scatter_stream."""
+    import torch
+
+    n_total = 7_000_000_000
+    comm = comm_cls(group_size=X, qgz_elems=QGZ_BUCKET, qgz_stages=1,
+                    qgz_cfg=zpp.QuantConfig(bit_width=4, block_size=512))
+    full, tail, tail_pad, n_out = comm.stream_layout(n_total)
+    grads = torch.empty(n_total, dtype=torch.bfloat16, device=dev)
+    for b in range(full + 1):
+        lo = b * QGZ_BUCKET
+        synth.device(2000 + 1000 * rank + b, 0, min(QGZ_BUCKET, n_total - lo), torch.bfloat16, "grad",
+                     out=grads[lo:lo + QGZ_BUCKET])
+    out = torch.empty(n_out, dtype=torch.float32, device=dev)
+    t = timed(lambda: comm.qgz_reduce_scatter_stream(grads, out=out), max(2, min(steps // 5, 4)), 1)
+    comm.check()
+    per = QGZ_BUCKET // world
+    chk = bad = 0
+    for b in range(0, full, 13):  # a few buckets, and the padded tail
+        c, m = sampled.qgz_check(out[b * per:(b + 1) * per], rank, world, X, QGZ_BUCKET, seed_base=2000 + b,
+                                 samples=256, rng_seed=b)
+        chk, bad = chk + c, bad + m
+    c, m = sampled.qgz_check(out[full * per:], rank, world, X, tail_pad, seed_base=2000 + full, samples=512,
+                             valid=tail)
+    add_parity("qgz_stream", chk + c, bad + m)
+    comm.close()
+    del grads, out
+    torch.cuda.empty_cache()
+    wire_b, hbm_b = qgz_bytes(QGZ_BUCKET, world, X)
+    wire_t, hbm_t = qgz_bytes(tail_pad, world, X)
+    wire, hbm = full * wire_b + wire_t, full * hbm_b + hbm_t
+    t_roof = max(wire / (NVLINK_NOMINAL_GBS * 1e9), hbm / (hbm_peak * 1e9))
+    return {"workload": "qgZ INT4/512 over a 7B bf16 gradient stream: 52 x 256 MiB buckets + padded tail",
+            "params": n_total, "buckets": full, "tail": tail, "tail_padded": tail_pad, "groups": f"{world // X}x{X}",
+            "ms_per_step": t * 1e3, "effective_GBps": world * 2 * n_total / t / 1e9,
+            "busbw_GBps": 2 * n_total * (world - 1) / world / t / 1e9 if world > 1 else None,
+            "params_per_s": world * n_total / t,
+            "roofline": {"t_roof_ms": t_roof * 1e3, "frac": t_roof / t,
+                         "nvlink_frac_of_900": wire / t / 1e9 / NVLINK_NOMINAL_GBS if wire else None,
+                         "hbm_frac": hbm / t / 1e9 / hbm_peak},
+            "wire_bytes_per_gpu": wire, "bf16_reduce_scatter_wire_bytes_per_gpu": 2 * n_total * (world - 1) // world}
+
+
+def step_leg(*, world, rank, dev, timed, steps, oversub, comm_cls, zpp, synth, sampled, add_parity, nccl_allgather,
+             nccl_reduce_scatter):
+    """BASELINE configs[4]: the communication of a ZeRO++ step over a GPT-13B
+    layer stack (h = 5120, 40 layers; zs/engine.py:345-398 order): forward qwZ
+    (INT8/2048) layer by layer writing each layer's hpZ secondary, backward hpZ
+    gathers inside the group in reverse layer order, gradient qgZ (INT4/512,
+    S = 2) per layer -- with and without the cross-layer prefetch of the next
+    layer's quantization -- vs ZeRO-3's fp16 all-gather x2 + bf16
+    reduce-scatter per layer (NCCL)."""
     import torch
 
     X = min(world, 4)
     h = 5120
+    n_layers = 40
     layer = 12 * h * h + 13 * h
     layer_p = _pad(layer, world * 2048 * 4)
-    comm = comm_cls(group_size=X, qwz_shard=layer_p // world, hpz_sec=layer_p // X, qgz_elems=layer_p,
+    shard = layer_p // world
+    comm = comm_cls(group_size=X, qwz_shard=shard, hpz_sec=layer_p // X, hpz_layers=n_layers, qgz_elems=layer_p,
                     qgz_stages=2, qgz_cfg=zpp.QuantConfig(bit_width=4, block_size=512))
-    w = (torch.randn(layer_p // world, generator=g, device=dev) * 0.02).half()
-    gl = (torch.randn(layer_p, generator=g, device=dev) * 1e-3).bfloat16()
+    ws = [synth.device(3000 + 100 * i + rank, 0, shard, torch.float16, "weight", device=dev) for i in range(n_layers)]
+    g = synth.device(5000 + 1000 * rank, 0, layer_p, torch.bfloat16, "grad", device=dev)
     wout = torch.empty(layer_p, dtype=torch.float16, device=dev)
+    hout = torch.empty(layer_p, dtype=torch.float16, device=dev)
     gout = torch.empty(layer_p // world, dtype=torch.float32, device=dev)
 
-    def zeropp_layer():
-        comm.qwz_allgather(w, out=wout, write_secondary=True)
-        comm.hpz_allgather(out=wout)
-        comm.qgz_reduce_scatter(gl, out=gout)
+    def zeropp_step(prefetch):
+        for i in range(n_layers):  # forward
+            comm.qwz_allgather(ws[i], out=wout, write_secondary=True, layer=i,
+                               next_shard=ws[i + 1] if prefetch and i + 1 < n_layers else None)
+        for i in reversed(range(n_layers)):  # backward
+            comm.hpz_allgather(out=hout, layer=i)
+            comm.qgz_reduce_scatter(g, out=gout)
 
-    t = timed(zeropp_layer)
+    n_steps = max(2, min(steps // 5, 3))
+    t_pf = timed(lambda: zeropp_step(True), n_steps, 1)
+    t_no = timed(lambda: zeropp_step(False), n_steps, 1)
     comm.check()
+    # after the last step: wout = layer 39 (forward), hout = layer 0 (backward)
+    c1, b1 = sampled.qwz_check(wout, world, shard, seed_base=3000 + 100 * (n_layers - 1), samples=1024, rng_seed=rank)
+    c2, b2 = sampled.qwz_check(hout, world, shard, seed_base=3000, samples=1024, rng_seed=rank + 7)
+    c3, b3 = sampled.qgz_check(gout, rank, world, X, layer_p, stages=2, seed_base=5000, samples=1024)
+    add_parity("step_13b", c1 + c2 + c3, b1 + b2 + b3)
     comm.close()
-    res = {"workload": "fwd qwZ + bwd hpZ + grad qgZ of one GPT-13B layer", "layer_params": layer,
-           "padded": layer_p, "groups": f"{world // X}x{X}", "zeropp_ms": t * 1e3, "zeropp_40_layers_ms": 40e3 * t}
+    res = {"workload": "fwd qwZ (prefetched) + bwd hpZ + grad qgZ (S=2) over 40 GPT-13B layers", "layers": n_layers,
+           "layer_params": layer, "padded": layer_p, "groups": f"{world // X}x{X}",
+           "zeropp_ms": t_pf * 1e3, "zeropp_no_prefetch_ms": t_no * 1e3, "prefetch_gain": t_no / t_pf}
     if world > 1 and not oversub:
         bout = torch.empty(layer_p // world, dtype=torch.bfloat16, device=dev)
+        gb = g.clone()
 
-        def zero3_layer():
-            nccl_allgather(w, out=wout)
-            nccl_allgather(w, out=wout)
-            nccl_reduce_scatter(gl, out=bout)
+        def zero3_step():
+            for i in range(n_layers):
+                nccl_allgather(ws[i], out=wout)
+            for i in reversed(range(n_layers)):
+                nccl_allgather(ws[i], out=hout)
+                nccl_reduce_scatter(gb, out=bout)
 
-        t3 = timed(zero3_layer)
-        res.update({"zero3_nccl_ms": t3 * 1e3, "speedup_vs_zero3": t3 / t})
+        t3 = timed(zero3_step, n_steps, 1)
+        res.update({"zero3_nccl_ms": t3 * 1e3, "speedup_vs_zero3": t3 / t_pf})
+        del bout, gb
+    del ws, g, wout, hout, gout
+    torch.cuda.empty_cache()
     return res
 
 

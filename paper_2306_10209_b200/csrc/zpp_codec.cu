@@ -280,6 +280,20 @@ static int run_gather(const SrcTable& t, int n_src, int rot, int64_t shard_len, 
       return check_cuda(cudaGetLastError(), "dequant16_kernel launch");
     }
   }
+  if constexpr (sizeof(O) >= 4 && std::is_same<A, float>::value) {
+    // fp32 / f64 outputs, whole 16-byte code units, no write-through
+    constexpr int64_t E = 128 / BITS;
+    bool wide = vec_ok && sec_out == nullptr && shard_len % E == 0 && block % E == 0 &&
+                (out_stride == 0 || out_stride % E == 0);
+    for (int i = 0; i < n_src; ++i) wide = wide && aligned16(t.codes[i]);
+    if (wide) {
+      auto k = dequant_wide_kernel<BITS, O>;
+      const int grid = grid_for(k, 256, ceil_div(shard_len / E, 256));
+      k<<<grid, 256, 0, st>>>(t, n_src, shard_len, block, reinterpret_cast<O*>(out),
+                              out_stride ? out_stride : shard_len, flag);
+      return check_cuda(cudaGetLastError(), "dequant_wide_kernel launch");
+    }
+  }
   auto k = dequant_gather_kernel<BITS, A, O>;
   const int64_t tiles = ceil_div(ceil_div(shard_len, 8), 32 * 4) * n_src;
   const int grid = grid_for(k, 256, ceil_div(tiles, 8));

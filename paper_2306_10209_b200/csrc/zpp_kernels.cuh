@@ -869,6 +869,75 @@ dequant16_kernel(SrcTable src, int n_src, int rot, int64_t shard_len, int64_t B,
 }
 
 // ---------------------------------------------------------------------------
+// K4 (fp32 / f64 outputs), fp32 absmax, 16-byte code units: each element is
+// the reference's f64 product RN64(code * RN64(absmax/qmax)) (one DMUL, the
+// code made exact by the 2^52+2^51 trick), rounded once to the output type.
+// Lane = one unit (E = 16 INT8 or 32 INT4 elements); sources one after the
+// other, grid-stride over units; all-unit-aligned shards only (the host
+// guarantees shard_len % E == 0 and 16-byte aligned codes/output), no hpZ
+// write-through.  Replaces the 8-element exact kernel on these shapes
+// (config 1's fp32 round trip).
+template <int BITS, typename O>
+__global__ void __launch_bounds__(256)
+dequant_wide_kernel(SrcTable src, int n_src, int64_t shard_len, int64_t B, O* __restrict__ out, int64_t out_stride,
+                    uint32_t* __restrict__ flag) {
+  if (comm_aborted(flag)) return;
+  constexpr int E = Unit16B<BITS>::E;
+  const int64_t units = shard_len / E;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const bool pow2 = (B & (B - 1)) == 0;
+  const int lg = pow2 ? __ffsll(B) - 1 : 0;
+  bool bad = false;
+  for (int s = 0; s < n_src; ++s) {
+    const uint4* cs = reinterpret_cast<const uint4*>(src.codes[s]);
+    const float* am = reinterpret_cast<const float*>(src.absmax[s]);
+    O* o = out + (int64_t)s * out_stride;
+    for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < units; u += stride) {
+      const uint4 w = __ldg(cs + u);
+      bad |= bad_codes(w, BITS);
+      const int64_t e0 = u * E;
+      const double sc = scale_of<BITS>((double)__ldg(am + (pow2 ? (e0 >> lg) : e0 / B)));
+      const uint32_t* ww = reinterpret_cast<const uint32_t*>(&w);
+      double v[E];
+      if constexpr (BITS == 8) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint32_t b = ww[k] ^ 0x80808080u;
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            v[4 * k + j] = __dmul_rn(__dsub_rn(__hiloint2double(0x43380000, (int)__byte_perm(b, 0, 0x4440 + j)),
+                                               Bias<8>::kD), sc);
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint32_t b = ww[k] ^ 0x88888888u;
+          const uint32_t ev = b & 0x0F0F0F0Fu, od = (b >> 4) & 0x0F0F0F0Fu;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            v[8 * k + 2 * j] = __dmul_rn(
+                __dsub_rn(__hiloint2double(0x43380000, (int)__byte_perm(ev, 0, 0x4440 + j)), Bias<4>::kD), sc);
+            v[8 * k + 2 * j + 1] = __dmul_rn(
+                __dsub_rn(__hiloint2double(0x43380000, (int)__byte_perm(od, 0, 0x4440 + j)), Bias<4>::kD), sc);
+          }
+        }
+      }
+      O* dst = o + e0;
+      if constexpr (sizeof(O) == 4) {
+#pragma unroll
+        for (int i = 0; i < E / 4; ++i)
+          reinterpret_cast<float4*>(dst)[i] = make_float4(__double2float_rn(v[4 * i]), __double2float_rn(v[4 * i + 1]),
+                                                          __double2float_rn(v[4 * i + 2]), __double2float_rn(v[4 * i + 3]));
+      } else {
+#pragma unroll
+        for (int i = 0; i < E / 2; ++i) reinterpret_cast<double2*>(dst)[i] = make_double2(v[2 * i], v[2 * i + 1]);
+      }
+    }
+  }
+  if (bad) raise_flag(flag, FLAG_BADCODE);
+}
+
+// ---------------------------------------------------------------------------
 // K4 over NVLink, TMA variant: one elected thread streams TILE-byte tiles of
 // codes from the (peer) source with cp.async.bulk into a STAGES-deep shared
 // ring, completion tracked by mbarrier transaction counts; all 256 threads
