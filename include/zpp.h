@@ -202,6 +202,18 @@ int zpp_qgz_reduce_scatter(zpp_comm_t comm, size_t sym_offset, const void* grad,
                            int intra_bits, int64_t intra_block, int inter_bits, int64_t inter_block, void* out,
                            int out_dtype, void* errflag, void* stream);
 
+/* qgZ over n_buckets consecutive buckets of n elements each (a gradient
+ * stream cut into buckets, BASELINE configs[3]; zs/engine.py:455-506 reduces
+ * a model's gradients this way): bucket b is one zpp_qgz_reduce_scatter of
+ * grad[b*n, (b+1)*n) into out[b*n/W, (b+1)*n/W).  Same results as n_buckets
+ * separate calls; K1 (quantize, hop-1 push) of bucket b+1 runs on the
+ * communicator's side stream beside K2/K3 of bucket b.  No reference
+ * counterpart beyond the per-bucket qgz_2hop (zs/collectives.py:464-569). */
+int zpp_qgz_reduce_scatter_buckets(zpp_comm_t comm, size_t sym_offset, const void* grad, int dtype, int64_t n,
+                                   int n_buckets, int stages, int reorder, int intra_bits, int64_t intra_block,
+                                   int inter_bits, int64_t inter_block, void* out, int out_dtype, void* errflag,
+                                   void* stream);
+
 /* symmetric-workspace bytes each fused collective needs at its sym_offset
  * (double-buffered; 256-byte aligned regions) */
 size_t zpp_qwz_sym_bytes(int64_t shard_len, int bits, int64_t block, int world);

@@ -62,6 +62,8 @@ SIGNATURES = {
     "zpp_hpz_allgather": (c_int, [P, c_size_t, c_int64, c_int, P, P, P]),
     "zpp_qgz_reduce_scatter": (c_int, [P, c_size_t, P, c_int, c_int64, c_int, c_int, c_int, c_int64, c_int,
                                        c_int64, P, c_int, P, P]),
+    "zpp_qgz_reduce_scatter_buckets": (c_int, [P, c_size_t, P, c_int, c_int64, c_int, c_int, c_int, c_int, c_int64,
+                                               c_int, c_int64, P, c_int, P, P]),
     "zpp_qwz_sym_bytes": (c_size_t, [c_int64, c_int, c_int64, c_int]),
     "zpp_qgz_sym_bytes": (c_size_t, [c_int64, c_int, c_int, c_int, c_int64, c_int, c_int64]),
     "zpp_hpz_sym_bytes": (c_size_t, [c_int64, c_int]),

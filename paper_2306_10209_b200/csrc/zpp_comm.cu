@@ -362,12 +362,20 @@ int zpp_qwz_allgather(zpp_comm_t c, size_t sym_offset, const void* shard, int dt
 // after this rank passed barrier(i).  The next call finds the prefetched
 // shard by (pointer, length, config, offset) and waits for it instead of
 // quantizing; any other shard waits for it and is quantized as usual.
-static int qwz_sms_for_prefetch() {
+// SM budget of the prefetched K0: it must finish under the gather it hides
+// behind.  K0 moves ~3 HBM bytes per element at ~6.3 TB/s on the whole GPU;
+// the gather pulls (W-1) code bytes per element at ~640 GB/s, so K0 needs
+// about 0.3/(W-1) of the SMs; 0.4/(W-1) leaves margin (W = 2: 59 SMs,
+// W = 4: 20, W = 8: 8).  A fixed sm_count/6 made the prefetch slower than
+// the gather at W = 2 and the 40-layer step 14% slower than no prefetch.
+static int qwz_sms_for_prefetch(int world) {
   static const int v = [] {
     const char* e = getenv("ZPP_QWZ_PREFETCH_SMS");
     return e ? atoi(e) : 0;
   }();
-  return v > 0 ? v : std::max(8, sm_count() / 6);
+  if (v > 0) return v;
+  const int s = (int)(sm_count() * 0.4 / std::max(1, world - 1) + 0.5);
+  return std::min(std::max(8, s), sm_count() / 2);
 }
 
 int zpp_qwz_allgather_next(zpp_comm_t c, size_t sym_offset, const void* shard, int dtype, int64_t shard_len,
@@ -440,7 +448,7 @@ int zpp_qwz_allgather_next(zpp_comm_t c, size_t sym_offset, const void* shard, i
     AddrSpec a;
     a.n = next_len;
     {
-      SmBudget budget(qwz_sms_for_prefetch());
+      SmBudget budget(qwz_sms_for_prefetch(c->world));
       rc = launch_quantize(next_shard, dtype, a, next_len, bits, block, c->local + nbase, c->local + nbase + nabs, flag,
                            c->side);
     }
@@ -461,7 +469,7 @@ int zpp_qwz_allgather_next(zpp_comm_t c, size_t sym_offset, const void* shard, i
     absmax[r] = c->peers[r] + base + abs_off;
   }
   {
-    SmBudget budget(prefetch ? sm_count() - qwz_sms_for_prefetch() : 0);
+    SmBudget budget(prefetch ? sm_count() - qwz_sms_for_prefetch(c->world) : 0);
     rc = launch_gather_dequant(codes, absmax, dtype == ZPP_F64 ? ZPP_F64 : ZPP_F32, c->world, c->rank, shard_len,
                                bits, block, out, out_dtype, sec_out, sec_lo, sec_len, flag, st, out_stride);
   }
@@ -545,12 +553,21 @@ size_t zpp_qgz_sym_bytes(int64_t n, int world, int stages, int intra_bits, int64
 int zpp_qgz_reduce_scatter(zpp_comm_t c, size_t sym_offset, const void* grad, int dtype, int64_t n, int stages,
                            int reorder, int intra_bits, int64_t intra_block, int inter_bits, int64_t inter_block,
                            void* out, int out_dtype, void* errflag, void* stream) {
+  return zpp_qgz_reduce_scatter_buckets(c, sym_offset, grad, dtype, n, 1, stages, reorder, intra_bits, intra_block,
+                                        inter_bits, inter_block, out, out_dtype, errflag, stream);
+}
+
+int zpp_qgz_reduce_scatter_buckets(zpp_comm_t c, size_t sym_offset, const void* grad, int dtype, int64_t n,
+                                   int n_buckets, int stages, int reorder, int intra_bits, int64_t intra_block,
+                                   int inter_bits, int64_t inter_block, void* out, int out_dtype, void* errflag,
+                                   void* stream) {
   int rc = comm_ok(c);
   if (rc) return rc;
   if ((intra_bits != 4 && intra_bits != 8) || (inter_bits != 4 && inter_bits != 8) || intra_block < 8 ||
       intra_block % 8 || inter_block < 8 || inter_block % 8)
     return fail(ZPP_ERR_CONFIG, "bad quant config");
   if (stages < 1) return fail(ZPP_ERR_VALIDATION, "stages must be >= 1");
+  if (n_buckets < 1) return fail(ZPP_ERR_VALIDATION, "n_buckets must be >= 1");
   const int W = c->world, X = c->group, Y = W / X;
   if (n < 0 || n % ((int64_t)stages * W)) return fail(ZPP_ERR_VALIDATION, "input length not divisible by stages*world");
   const QgzLayout l = qgz_layout(n, W, Y, stages, intra_bits, intra_block, inter_bits, inter_block);
@@ -567,7 +584,18 @@ int zpp_qgz_reduce_scatter(zpp_comm_t c, size_t sym_offset, const void* grad, in
   const size_t out_esz = out_dtype == ZPP_F64 ? 8 : (out_dtype == ZPP_F32 ? 4 : 2);
   const int64_t L = l.L;
   const int64_t msg_elems = (int64_t)Y * L;  // one hop-1 message
-  const bool pipelined = stages > 1;
+  const size_t in_esz = dtype == ZPP_F64 ? 8 : (dtype == ZPP_F32 ? 4 : 2);
+  // Work units u = (bucket b, stage s), b-major: K1 of unit u+1 runs on the
+  // side stream beside K2/K3 of unit u.  Buckets are independent qgz_2hop
+  // calls (bucket b: grad[b*n, (b+1)*n) -> out[b*n/W, (b+1)*n/W)); pipelining
+  // them needs no extra barrier, unlike stages of one bucket.
+  // ZPP_QGZ_XB=0 runs buckets back to back without overlap (A/B).
+  static const int xb_env = [] {
+    const char* e = getenv("ZPP_QGZ_XB");
+    return e ? atoi(e) : 1;
+  }();
+  const int units = n_buckets * stages;
+  const bool pipelined = stages > 1 || (n_buckets > 1 && xb_env != 0);
   if (pipelined && !c->ev_start) {
     if (!c->side) rc = check_cuda(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking), "side stream");
     if (!rc) rc = check_cuda(cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming), "event");
@@ -584,15 +612,28 @@ int zpp_qgz_reduce_scatter(zpp_comm_t c, size_t sym_offset, const void* grad, in
   trace_reset(c);
   trace_mark(c, TR_BEGIN, st);
   const uint64_t use0 = c->qgz_uses;
-  c->qgz_uses += stages;
-  auto base_of = [&](int s) { return sym_offset + ((use0 + s) & 1) * l.region; };
+  c->qgz_uses += units;
+  auto base_of = [&](int u) { return sym_offset + ((use0 + u) & 1) * l.region; };
+  // unit u = (bucket u / stages, stage u % stages) writes out[u*L, (u+1)*L):
+  // bucket b's partition (n/W = stages*L elements) follows bucket b-1's
+  auto out_of = [&](int u) { return reinterpret_cast<uint8_t*>(out) + (size_t)u * L * out_esz; };
   // K1: swizzle + quantize stage s's slices into my send buffer [j][c][e]
   // SM split while K1(s+1) runs beside K2(s) (pipelined only)
   static const int k1_sms_env = [] {
     const char* e = getenv("ZPP_QGZ_K1_SMS");
     return e ? atoi(e) : 0;
   }();
-  const int k1_sms = pipelined ? (k1_sms_env > 0 ? k1_sms_env : sm_count() / 3) : 0;
+  static const int k1_xb_sms_env = [] {
+    const char* e = getenv("ZPP_QGZ_K1_XB_SMS");
+    return e ? atoi(e) : 0;
+  }();
+  // SMs (resident-CTA budget) of the K1 running beside a K2/K3: a third when
+  // overlapping stages of one bucket (K2/K3 of a stage are short), a larger
+  // share across buckets (K1 and the fold are both issue-bound; swept in
+  // tools/qgz_xb_sweep.sh)
+  const int k1_sms = !pipelined ? 0
+                     : stages > 1 ? (k1_sms_env > 0 ? k1_sms_env : sm_count() / 3)
+                                  : (k1_xb_sms_env > 0 ? k1_xb_sms_env : sm_count() / 2);
   // Hop 1 either
   //  * push: K1 (quantize_push_kernel) streams each message into the receiving
   //    peer's [src_loc][c][e] region with TMA bulk stores while it quantizes,
@@ -619,8 +660,10 @@ int zpp_qgz_reduce_scatter(zpp_comm_t c, size_t sym_offset, const void* grad, in
                     ((intra_block / epl) & (intra_block / epl - 1)) == 0;
   if (push && (reinterpret_cast<uintptr_t>(grad) & 15))
     return fail(ZPP_ERR_VALIDATION, "qgZ: the gradient buffer must be 16-byte aligned");
-  auto k1 = [&](int s, cudaStream_t on) {
-    SmBudget budget(s > 0 ? k1_sms : 0);  // K1(0) runs alone
+  auto k1 = [&](int u, cudaStream_t on) {
+    SmBudget budget(u > 0 ? k1_sms : 0);  // K1(0) runs alone
+    const int s = u % stages;
+    const void* g = reinterpret_cast<const uint8_t*>(grad) + (size_t)(u / stages) * n * in_esz;
     AddrSpec a;
     a.swizzle = true;
     a.L = L;
@@ -629,7 +672,7 @@ int zpp_qgz_reduce_scatter(zpp_comm_t c, size_t sym_offset, const void* grad, in
     a.X = X;
     a.Y = Y;
     a.reorder = reorder ? 1 : 0;
-    const size_t base = base_of(s);
+    const size_t base = base_of(u);
     if (push) {
       uint8_t* dc[kMaxPush];
       uint8_t* da[kMaxPush];
@@ -641,12 +684,12 @@ int zpp_qgz_reduce_scatter(zpp_comm_t c, size_t sym_offset, const void* grad, in
       bool handled = false;
       // rank loc starts with the message for local peer loc+1: the group's
       // ranks begin on different destinations
-      const int rc1 = launch_quantize_push(grad, dtype, a, (int64_t)W * L, intra_bits, intra_block, dc, da, msg_blocks,
+      const int rc1 = launch_quantize_push(g, dtype, a, (int64_t)W * L, intra_bits, intra_block, dc, da, msg_blocks,
                                            (loc + 1) % X, flag, on, &handled);
       if (rc1 || handled) return rc1;
       return fail(ZPP_ERR_VALIDATION, "qgZ: no push path for this shape");
     }
-    return launch_quantize(grad, dtype, a, (int64_t)W * L, intra_bits, intra_block, c->local + base + l.send_codes,
+    return launch_quantize(g, dtype, a, (int64_t)W * L, intra_bits, intra_block, c->local + base + l.send_codes,
                            c->local + base + l.send_abs, flag, on);
   };
   if (pipelined) {
@@ -658,8 +701,9 @@ int zpp_qgz_reduce_scatter(zpp_comm_t c, size_t sym_offset, const void* grad, in
     if ((rc = k1(0, c->side))) return rc;
     if ((rc = check_cuda(cudaEventRecord(c->ev_k1, c->side), "record"))) return rc;
   }
-  for (int s = 0; s < stages; ++s) {
+  for (int s = 0; s < units; ++s) {
     const size_t base = base_of(s);
+    uint8_t* const out_s = out_of(s);
     if (pipelined) {
       if ((rc = check_cuda(cudaStreamWaitEvent(st, c->ev_k1, 0), "wait"))) return rc;
     } else if ((rc = k1(s, st))) {
@@ -669,13 +713,13 @@ int zpp_qgz_reduce_scatter(zpp_comm_t c, size_t sym_offset, const void* grad, in
     rc = barrier(c, 1, kBarrierTimeoutMs, flag, st);
     if (rc) return rc;
     trace_mark(c, TR_BARRIER, st);
-    if (pipelined && s + 1 < stages) {
+    if (pipelined && s + 1 < units) {
       if ((rc = check_cuda(cudaEventRecord(c->ev_bar, st), "record"))) return rc;
       if ((rc = check_cuda(cudaStreamWaitEvent(c->side, c->ev_bar, 0), "wait"))) return rc;
       if ((rc = k1(s + 1, c->side))) return rc;
       if ((rc = check_cuda(cudaEventRecord(c->ev_k1, c->side), "record"))) return rc;
     }
-    SmBudget budget(pipelined && s + 1 < stages ? sm_count() - k1_sms : 0);
+    SmBudget budget(pipelined && s + 1 < units ? sm_count() - k1_sms : 0);
     // K2: the X messages for this rank, ascending local source -- pushed into
     // this rank's receive region by the group's K1s, or pulled from the peers
     const void* codes[kMaxRanks];
@@ -696,7 +740,7 @@ int zpp_qgz_reduce_scatter(zpp_comm_t c, size_t sym_offset, const void* grad, in
       if (in_abs == ZPP_F32 && !push)
         rc = launch_drq_tma(codes, absmax, X, msg_elems, intra_bits, intra_block, inter_bits, inter_block, nullptr,
                             reinterpret_cast<double*>(c->local + base + l.hop_abs),
-                            reinterpret_cast<uint8_t*>(out) + (size_t)s * L * out_esz, out_dtype, flag, st, &handled);
+                            out_s, out_dtype, flag, st, &handled);
       if (rc) return rc;
       if (handled) {
         trace_mark(c, TR_K2, st);
@@ -704,7 +748,7 @@ int zpp_qgz_reduce_scatter(zpp_comm_t c, size_t sym_offset, const void* grad, in
       }
       rc = launch_drq_final(codes, absmax, in_abs, X, msg_elems, intra_bits, intra_block, inter_bits, inter_block,
                             reinterpret_cast<double*>(c->local + base + l.hop_abs),
-                            reinterpret_cast<uint8_t*>(out) + (size_t)s * L * out_esz, out_dtype, flag, st, &handled);
+                            out_s, out_dtype, flag, st, &handled);
       if (rc) return rc;
       if (handled) {
         trace_mark(c, TR_K2, st);
@@ -735,11 +779,11 @@ int zpp_qgz_reduce_scatter(zpp_comm_t c, size_t sym_offset, const void* grad, in
     }
     handled = false;
     rc = launch_dr_tma(codes, absmax, Y, L, inter_bits, inter_block,
-                       reinterpret_cast<uint8_t*>(out) + (size_t)s * L * out_esz, out_dtype, flag, st, &handled);
+                       out_s, out_dtype, flag, st, &handled);
     if (rc) return rc;
     if (!handled)
       rc = launch_dequant_reduce(codes, absmax, ZPP_F64, Y, L, inter_bits, inter_block,
-                                 reinterpret_cast<uint8_t*>(out) + (size_t)s * L * out_esz, out_dtype, 1.0, flag,
+                                 out_s, out_dtype, 1.0, flag,
                                  st, /*validate=*/false);
     if (rc) return rc;
     trace_mark(c, TR_K3, st);

@@ -375,13 +375,28 @@ __device__ __forceinline__ void quant_compute(const T* __restrict__ x, const Tea
   if constexpr (DEFER && BITS == 4) {
     if (!__any_sync(0xffffffffu, slow)) {
       general = false;
+      if (__all_sync(0xffffffffu, active)) {
+        // every team of the warp holds a block (all but the grid's last
+        // wave): unconditional stores from one hoisted base address, no
+        // per-chunk branch region
+        uint8_t* const ob = out + tl * BITS;
 #pragma unroll
-      for (int c = 0; c < CH; ++c) {
-        float v[8];
-        uint32_t q[8];
-        Raw<T>::to_float(raw[c], v);
-        if (quant_chunk_fast<QMAX>(v, inv32, q)) need |= 1u << c;
-        if (active) store_codes8<BITS>(out + (c * LANES + tl) * BITS, q);
+        for (int c = 0; c < CH; ++c) {
+          float v[8];
+          uint32_t q[8];
+          Raw<T>::to_float(raw[c], v);
+          if (quant_chunk_fast<QMAX>(v, inv32, q)) need |= 1u << c;
+          store_codes8<BITS>(ob + c * LANES * BITS, q);
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < CH; ++c) {
+          float v[8];
+          uint32_t q[8];
+          Raw<T>::to_float(raw[c], v);
+          if (quant_chunk_fast<QMAX>(v, inv32, q)) need |= 1u << c;
+          if (active) store_codes8<BITS>(out + (c * LANES + tl) * BITS, q);
+        }
       }
     }
   }
@@ -1530,9 +1545,7 @@ __device__ __forceinline__ void drq_team(const Src& src, int n_src, int64_t n, i
       }
     }
   }
-  double mx = 0.0;
-#pragma unroll
-  for (int i = 0; i < 16; ++i) mx = dmax_nn(mx, fabs(acc[i]));
+  double mx = absmax16(acc);
 #pragma unroll
   for (int off = LANES / 2; off >= 1; off >>= 1) mx = dmax_nn(mx, __shfl_xor_sync(0xffffffffu, mx, off));
   if (b < n_blocks_out && tl == 0) {
@@ -1643,9 +1656,7 @@ __device__ __forceinline__ void drq_epilogue(const double (&acc)[16], int64_t b,
                                              uint32_t* __restrict__ flag, FO* __restrict__ final_out,
                                              float* fo_tbl = nullptr) {
   constexpr int QMAX = Codes<OBITS>::kQmax;
-  double mx = 0.0;
-#pragma unroll
-  for (int i = 0; i < 16; ++i) mx = dmax_nn(mx, fabs(acc[i]));
+  double mx = absmax16(acc);
 #pragma unroll
   for (int off = 16; off >= 1; off >>= 1) mx = dmax_nn(mx, __shfl_xor_sync(0xffffffffu, mx, off));
   if (tl == 0) {

@@ -342,7 +342,9 @@ class Communicator:
         output is the concatenation of its partitions of every bucket.  The
         tail bucket is zero-padded as zs/engine.py:465-466 pads the whole
         tensor (one device copy into a staging buffer kept by the
-        communicator).  Buckets run back to back on the caller's stream."""
+        communicator).  The full buckets are one zpp_qgz_reduce_scatter_buckets
+        call: K1 of bucket b+1 runs on the communicator's side stream beside
+        K2/K3 of bucket b (same results as separate calls)."""
         self._usable()
         n_total = int(grads.numel())
         full, tail, tail_pad, n_out = self.stream_layout(n_total)
@@ -351,9 +353,12 @@ class Communicator:
             out = torch.empty(n_out, dtype=out_dtype, device=grads.device)
         _check_buf(out, "out", n_out)
         bucket, w = self.qgz_elems, self.world
-        for b in range(full):
-            self._qgz(grads[b * bucket:(b + 1) * bucket], bucket, out[b * bucket // w:(b + 1) * bucket // w],
-                      out.dtype, reorder)
+        if full:
+            _lib.check(self.lib.zpp_qgz_reduce_scatter_buckets(
+                self.handle, self.layout.qgz, grads.data_ptr(), dtype_code(grads.dtype), bucket, full,
+                self.qgz_stages, int(reorder), self.qgz_intra_cfg.bit_width, self.qgz_intra_cfg.block_size,
+                self.qgz_cfg.bit_width, self.qgz_cfg.block_size, out.data_ptr(), dtype_code(out.dtype),
+                self.flag.data_ptr(), stream_ptr()), "qgz_reduce_scatter_stream")
         if tail:
             if getattr(self, "_tail_buf", None) is None or self._tail_buf.numel() != tail_pad \
                     or self._tail_buf.dtype != grads.dtype:

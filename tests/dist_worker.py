@@ -181,32 +181,35 @@ def main():
     comm3.close()
 
     # ---- bucketed gradient stream with a zero-padded tail (configs[3]) --------
-    S2 = 1
-    bucket = S2 * world * 2048
-    n_stream = 2 * bucket + 3 * 512 + 77  # two buckets and a ragged tail
-    gs_host = [bf16_bits(np.random.default_rng(700 + r).normal(size=n_stream) * 1e-3) for r in range(world)]
-    comm4 = Communicator(group_size=X, qgz_elems=bucket, qgz_stages=S2,
-                         qgz_cfg=zpp.QuantConfig(bit_width=4, block_size=512))
-    full, tail, tail_pad, n_out = comm4.stream_layout(n_stream)
-    check("stream layout", full == 2 and tail == 3 * 512 + 77 and tail_pad % (world * 512) == 0)
-    want_parts = []
-    for b in range(full + 1):
-        lo_b = b * bucket
-        hi_b = min(lo_b + bucket, n_stream)
-        nb = bucket if b < full else tail_pad
-        srcs = []
-        for r in range(world):
-            v = np.zeros(nb)
-            v[:hi_b - lo_b] = gu.as_f64(gs_host[r][lo_b:hi_b], "bf16")
-            srcs.append(v)
-        want_parts.append(O.qgz_2hop(srcs, X, Y, S2, 4, 512)[rank])
-    want_s = np.concatenate(want_parts)
-    gts = gu.to_torch(gs_host[rank], "bf16")
-    for it in range(2):
-        o_s = comm4.qgz_reduce_scatter_stream(gts, out_dtype=torch.float64)
-        comm4.check()
-        check(f"qgz stream it{it}", o_s.numel() == n_out and same_bits(o_s.cpu().numpy(), want_s))
-    comm4.close()
+    # five buckets (one zpp_qgz_reduce_scatter_buckets call: K1 of bucket b+1
+    # beside K2/K3 of bucket b) and a ragged tail, with 1 and 2 stages per bucket
+    for S2 in (1, 2):
+        bucket = S2 * world * 2048
+        n_stream = 5 * bucket + 3 * 512 + 77
+        gs_host = [bf16_bits(np.random.default_rng(700 + 10 * S2 + r).normal(size=n_stream) * 1e-3)
+                   for r in range(world)]
+        comm4 = Communicator(group_size=X, qgz_elems=bucket, qgz_stages=S2,
+                             qgz_cfg=zpp.QuantConfig(bit_width=4, block_size=512))
+        full, tail, tail_pad, n_out = comm4.stream_layout(n_stream)
+        check("stream layout", full == 5 and tail == 3 * 512 + 77 and tail_pad % (world * S2 * 512) == 0)
+        want_parts = []
+        for b in range(full + 1):
+            lo_b = b * bucket
+            hi_b = min(lo_b + bucket, n_stream)
+            nb = bucket if b < full else tail_pad
+            srcs = []
+            for r in range(world):
+                v = np.zeros(nb)
+                v[:hi_b - lo_b] = gu.as_f64(gs_host[r][lo_b:hi_b], "bf16")
+                srcs.append(v)
+            want_parts.append(O.qgz_2hop(srcs, X, Y, S2, 4, 512)[rank])
+        want_s = np.concatenate(want_parts)
+        gts = gu.to_torch(gs_host[rank], "bf16")
+        for it in range(2):
+            o_s = comm4.qgz_reduce_scatter_stream(gts, out_dtype=torch.float64)
+            comm4.check()
+            check(f"qgz stream S={S2} it{it}", o_s.numel() == n_out and same_bits(o_s.cpu().numpy(), want_s))
+        comm4.close()
 
     # ---- process groups for the staged comparators ---------------------------
     mine_pg, cross_pg = make_groups(X)

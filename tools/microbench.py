@@ -46,6 +46,8 @@ def main():
     lib = _lib.load()
     st = torch.cuda.current_stream().cuda_stream
     flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    if only == "fused":
+        return fused_n1(lib, st, flag)
     cases = [(torch.float16, 1_300_004_864, 8, 2048), (torch.float32, 1 << 24, 8, 2048),
              (torch.bfloat16, 134_217_728, 4, 512), (torch.float16, 134_217_728, 8, 2048)]
     if only == "qgz":
@@ -83,6 +85,28 @@ def main():
         qgz_shape(lib, st, flag, X, Y)
     torch.cuda.synchronize()
     print("flag", int(flag.item()))
+
+
+def fused_n1(lib, st, flag):
+    """The N = 1 qwZ step (one fused quantize -> dequantize pass over the 1.3B
+    fp16 buffer) on two input distributions: torch.randn * 0.02 and the
+    bench's counter-based synthetic weights (oracle/synth.py), 20 back-to-back
+    launches each, like bench.py's timed region."""
+    from oracle import synth
+    from paper_2306_10209_b200.dist import Communicator
+
+    M = 1_300_004_864
+    comm = Communicator(group_size=1, qwz_shard=M, qwz_cfg=zpp.QuantConfig(bit_width=8, block_size=2048))
+    out = torch.empty(M, dtype=torch.float16, device="cuda")
+    for name, mk in (("randn*0.02", lambda: (torch.randn(M, device="cuda") * 0.02).half()),
+                     ("synth", lambda: synth.device(1000, 0, M, torch.float16, "weight", device=torch.device("cuda")))):
+        x = mk()
+        t = timeit(lambda: comm.qwz_allgather(x, out=out), iters=20, warm=5)
+        report(f"fused N=1 qwZ pass, {name}", t, 5 * M + M // 2048 * 4)
+        del x
+        torch.cuda.empty_cache()
+    comm.check()
+    comm.close()
 
 
 def qgz_shape(lib, st, flag, X, Y):

@@ -7,9 +7,9 @@ N=${N:-4}; X=${X:-$N}; O=${OUT:-gpurun_out}; PORT=${PORT:-29561}
 mkdir -p $O
 export WORLD_SIZE=$N MASTER_ADDR=127.0.0.1 MASTER_PORT=$PORT
 for r in $(seq 1 $((N - 1))); do
-  RANK=$r LOCAL_RANK=$r timeout 600 python tools/nvl_profile.py $X > $O/nvl_rank$r.log 2>&1 &
+  RANK=$r LOCAL_RANK=$r timeout ${NCU_TIMEOUT:-600} python tools/nvl_profile.py $X > $O/nvl_rank$r.log 2>&1 &
 done
-RANK=0 LOCAL_RANK=0 timeout 600 ncu --set full --clock-control none --import-source on \
+RANK=0 LOCAL_RANK=0 timeout ${NCU_TIMEOUT:-600} ncu --set full --clock-control none --import-source on \
   --metrics nvlrx__bytes.sum,nvltx__bytes.sum,dram__bytes_read.sum,dram__bytes_write.sum \
   -k regex:"dequant16_tma_kernel|drq_tma_kernel|dr_tma_kernel|quantize_push_kernel|drq_tbl_kernel|quantize_reg_kernel" \
   --launch-skip ${SKIP:-8} --launch-count ${COUNT:-4} -o $O/nvl_n${N}_x${X} -f python tools/nvl_profile.py $X > $O/nvl_rank0.log 2>&1

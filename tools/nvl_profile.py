@@ -22,10 +22,16 @@ from paper_2306_10209_b200.dist import Communicator  # noqa: E402
 BUCKET = 134_217_728
 
 
+def say(msg):
+    print(f"[rank {os.environ.get('RANK')}] {msg}", flush=True)
+
+
 def main():
     local = int(os.environ.get("LOCAL_RANK", 0))
     torch.cuda.set_device(local)
+    say("init")
     dist.init_process_group("gloo")
+    say("gloo up")
     rank, world = dist.get_rank(), dist.get_world_size()
     X = int(sys.argv[1]) if len(sys.argv) > 1 else world
     dev = torch.device("cuda", local)
@@ -42,14 +48,18 @@ def main():
         torch.cuda.synchronize()
         dist.barrier()
 
+    say("inputs ready")
     for _ in range(2):  # warm-up (not profiled: ncu -k filters + launch skip in ncu_rank0.sh)
         comm.qwz_allgather(w, out=out)
         comm.qgz_reduce_scatter(g, out=part)
     fence()
+    say("warm-up done")
     comm.qwz_allgather(w, out=out)
     fence()
+    say("gather done")
     comm.qgz_reduce_scatter(g, out=part)
     fence()
+    say("qgz done")
     comm.check()
     comm.close()
     dist.destroy_process_group()
