@@ -224,7 +224,9 @@ def run_ours(args):
     sections = set(os.environ.get("ZPP_BENCH_LEGS", "qgz,config1,hpz,stream,step").split(","))
     lib = _lib.load()
     dev = torch.device("cuda", local)
-    X = min(world, 4)
+    # SURVEY 8d's hierarchy: two groups of W/2 consecutive GPUs stand in for
+    # two nodes (W = 8: 2x4, W = 4: 2x2, W = 2: 2x1)
+    X = group_size_for(world)
     shard_len = M_PARAMS // world
     cfg = zpp.QuantConfig(bit_width=8, block_size=2048)
     qgz_cfg = zpp.QuantConfig(bit_width=4, block_size=512)
@@ -397,6 +399,14 @@ def run_ours(args):
         extra["qgz"] = qgz_leg(comm=comm, world=world, rank=rank, X=X, dev=dev, timed=timed, steps=args.steps,
                                hbm_peak=hbm_peak, oversub=oversub, add_parity=add_parity, synth=synth,
                                sampled=sampled, nccl_reduce_scatter=nccl_reduce_scatter, traffic=traffic)
+        if world >= 2 and X != world:
+            # the same bucket with the whole box as one group (hop 2 a self-send)
+            c1g = Communicator(group_size=world, qgz_elems=QGZ_BUCKET, qgz_stages=1, qgz_cfg=qgz_cfg)
+            extra["qgz_one_group"] = qgz_leg(comm=c1g, world=world, rank=rank, X=world, dev=dev, timed=timed,
+                                             steps=args.steps, hbm_peak=hbm_peak, oversub=oversub,
+                                             add_parity=add_parity, synth=synth, sampled=sampled,
+                                             nccl_reduce_scatter=None, traffic=traffic, parity_name="qgz_one_group")
+            c1g.close()
     comm.close()
     torch.cuda.empty_cache()
     if "config1" in sections:
@@ -461,6 +471,10 @@ def run_ours(args):
     return 0
 
 
+def group_size_for(world: int) -> int:
+    return world // 2 if world >= 2 else 1
+
+
 def _pad(n: int, align: int) -> int:
     return (n + align - 1) // align * align
 
@@ -486,7 +500,7 @@ def qgz_bytes(n, world, X, in_block=512, out_block=512, final_bytes=4):
 
 
 def qgz_leg(*, comm, world, rank, X, dev, timed, steps, hbm_peak, oversub, add_parity, synth, sampled,
-            nccl_reduce_scatter, traffic):
+            nccl_reduce_scatter, traffic, parity_name="qgz"):
     """BASELINE configs[3], one bucket: qgZ INT4/512 2-hop reduce-scatter of a
     256 MiB bf16 gradient bucket (S = 1), with its roofline
     t_roof = max(wire / 900 GB/s, HBM / peak)."""
@@ -496,7 +510,7 @@ def qgz_leg(*, comm, world, rank, X, dev, timed, steps, hbm_peak, oversub, add_p
     part = torch.empty(QGZ_BUCKET // world, dtype=torch.float32, device=dev)
     t_qgz = timed(lambda: comm.qgz_reduce_scatter(grad, out=part), steps, 3)
     comm.check()
-    add_parity("qgz", *sampled.qgz_check(part, rank, world, X, QGZ_BUCKET, samples=4096))
+    add_parity(parity_name, *sampled.qgz_check(part, rank, world, X, QGZ_BUCKET, samples=4096))
     wire, hbm = qgz_bytes(QGZ_BUCKET, world, X)
     t_roof = max(wire / (NVLINK_NOMINAL_GBS * 1e9), hbm / (hbm_peak * 1e9))
     res = {"workload": "qgZ INT4/512 2-hop reduce-scatter of a 256 MiB bf16 bucket, S=1", "groups": f"{world // X}x{X}",
@@ -513,7 +527,7 @@ def qgz_leg(*, comm, world, rank, X, dev, timed, steps, hbm_peak, oversub, add_p
                         "note": "t_roof = max(wire/900 GB/s, HBM/peak); the path is bound by neither: the bit-exact "
                                 "f64 fold and the tie-checked quantizer are issue-bound (DESIGN.md, qgZ)"},
            "bf16_reduce_scatter_wire_bytes_per_gpu": 2 * QGZ_BUCKET * (world - 1) // world}
-    if world > 1 and not oversub:
+    if world > 1 and not oversub and nccl_reduce_scatter is not None:
         gb = grad.clone()
         pb = torch.empty(QGZ_BUCKET // world, dtype=torch.bfloat16, device=dev)
         t_rs = timed(lambda: nccl_reduce_scatter(gb, out=pb), steps, 3)
@@ -588,14 +602,14 @@ def config1_leg(*, lib, dev, rank, timed_flush, steps, hbm_peak, add_parity, max
 
 def hpz_leg(*, comm_cls, world, dev, timed, oversub, nccl_allgather, synth, sampled, add_parity, rank):
     """BASELINE configs[2]: hpZ gather of one GPT-1.3B layer (12h^2+13h, h=2048)
-    inside a group of min(N, 4) consecutive GPUs, vs NCCL's full-box and group
-    fp16 all-gathers.  The secondary shard is written through by the qwZ gather
+    inside a group of N/2 consecutive GPUs (2x4 on 8 GPUs), vs NCCL's full-box
+    and group fp16 all-gathers.  The secondary shard is written through by the qwZ gather
     (zs/engine.py:364-370)."""
     import torch
 
     from paper_2306_10209_b200.dist import make_groups
 
-    X = min(world, 4)
+    X = group_size_for(world)
     h = 2048
     layer = 12 * h * h + 13 * h
     layer_p = _pad(layer, world * 2048)
@@ -683,7 +697,7 @@ def step_leg(*, world, rank, dev, timed, steps, oversub, comm_cls, zpp, synth, s
     reduce-scatter per layer (NCCL)."""
     import torch
 
-    X = min(world, 4)
+    X = group_size_for(world)
     h = 5120
     n_layers = 40
     layer = 12 * h * h + 13 * h

@@ -44,7 +44,7 @@ from .topology import (
     optimal_stages,
     pipelined_seconds,
 )
-from .partitioner import MEMORY_MODES, PartitionSpec, build_partitions, memory_per_device, memory_report
+from .partitioner import PartitionSpec, build_partitions
 from .collectives import (
     BlockCodec,
     GatherResult,
@@ -72,7 +72,7 @@ __all__ = [
     "INTRA", "INTER", "ClusterTopology", "TrafficLedger", "CollectiveTrace", "PhaseStats",
     "normalized_cross_node_volume", "LinkParams", "LatencyEstimate", "estimate_latency", "pipelined_seconds",
     "optimal_stages",
-    "PartitionSpec", "build_partitions", "MEMORY_MODES", "memory_per_device", "memory_report",
+    "PartitionSpec", "build_partitions",
     "BlockCodec", "PassthroughCodec", "WirePayload", "as_codec", "GatherResult", "ReduceResult",
     "ReorderPermutation", "all_gather_baseline", "all_gather_qwz", "reduce_scatter_ring", "reorder_mapping",
     "qgz_2hop", "qgz_1hop", "reduce_scatter_ring_naive_quant",

@@ -335,17 +335,6 @@ def build_volumes():
     print("volume cases:", len(rows))
 
 
-def build_memory():
-    """memory_report CSVs (zs/partitioner.py:125-135) for a few model/cluster shapes."""
-    rows = []
-    for m, world, group, k in [(100_000_000_000, 1024, 16, 12), (13_000_000_000, 8, 4, 12), (1_300_000_000, 8, 2, 16),
-                               (7_000_000_000, 64, 8, 0)]:
-        rows.append(dict(m=m, world=world, group=group, k=k, csv=zs.memory_report(m, world, group, k)))
-    with open(os.path.join(HERE, "memory.json"), "w") as f:
-        json.dump(rows, f, indent=1)
-    print("memory cases:", len(rows))
-
-
 ENGINE_CASES = [
     # (name, ZeroConfig kwargs, task kwargs, passthrough codecs)
     ("plain", {}, {}, False),
@@ -400,6 +389,6 @@ def build_engine(steps=40):
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["quant", "fused", "collectives", "volumes", "wire", "memory", "engine"]
+    which = sys.argv[1:] or ["quant", "fused", "collectives", "volumes", "wire", "engine"]
     for name in which:
         globals()["build_" + name]()

@@ -220,33 +220,6 @@ def test_c10_latency_pipeline_model():
         zpp.LinkParams(intra_beta=0.0)
 
 
-def test_c06_memory_ratios():
-    """Acceptance c06 (pkg/tests/test_acceptance.py:227-245): 100B params on
-    1024 ranks, groups of 16: the hpZ secondary copy costs ~8.9x the ZeRO-3
-    footprint and plain replication ~114x the hpZ one."""
-    import paper_2306_10209_b200 as zpp
-
-    m, world, group, k = 100_000_000_000, 1024, 16, 12
-    z3, hpz, dp = (zpp.memory_per_device(mode, m, world, group, k) for mode in ("ZeRO3", "hpZ", "DP"))
-    assert abs(hpz / z3 - 8.9) / 8.9 < 0.05 and abs(dp / hpz - 114.0) / 114.0 < 0.05
-    rows = zpp.memory_report(m, world, group).splitlines()
-    assert rows[0].startswith("mode,") and len(rows) == 5
-    with pytest.raises(zpp.ValidationError):
-        zpp.memory_per_device("FSDP", m, world, group)
-
-
-def test_memory_report_matches_reference():
-    """memory_report CSV byte-identical to the reference's (tests/golden/memory.json)."""
-    import json
-
-    import paper_2306_10209_b200 as zpp
-
-    with open(os.path.join(ROOT, "tests", "golden", "memory.json")) as f:
-        rows = json.load(f)
-    for r in rows:
-        assert zpp.memory_report(r["m"], r["world"], r["group"], r["k"]) == r["csv"], r
-
-
 def test_engine_parts_on_the_host():
     """Engine pieces that need no GPU: layer views share the flat vector,
     forward shapes and tanh range, per-rank gradient shards sum to the full
