@@ -266,7 +266,7 @@ static int run_gather(const SrcTable& t, int n_src, int rot, int64_t shard_len, 
       int occ = 0;
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 256, smem);
       const int64_t units = ceil_div(shard_len, 128 / BITS);
-      const int grid = (int)std::min<int64_t>((int64_t)sm_budget() * std::max(occ, 1), ceil_div(units, TU) * n_src);
+      const int grid = (int)std::min<int64_t>((int64_t)sm_budget() * occ_capped(occ), ceil_div(units, TU) * n_src);
       k<<<grid, 256, smem, st>>>(t, n_src, rot, shard_len, block, reinterpret_cast<O*>(out),
                                  reinterpret_cast<O*>(sec_out), sec_lo, sec_len, vec_ok, flag, out_stride);
       return check_cuda(cudaGetLastError(), "dequant16_tma_kernel launch");

@@ -432,7 +432,20 @@ int zpp_qwz_allgather_next(zpp_comm_t c, size_t sym_offset, const void* shard, i
   if (rc) return rc;
   trace_mark(c, TR_BARRIER, st);
   // prefetch: K0 of the next shard into the next call's half, on the side
-  // stream, after this rank passed barrier(i); only for an unchanged layout
+  // stream, after this rank passed barrier(i); only for an unchanged layout.
+  // Default ("share"): both grids span every SM -- the gather capped at
+  // ZPP_QWZ_GATHER_OCC (2) CTAs per SM, which leaves room for one CTA of K0
+  // per SM, so K0 runs in the issue slots the NVLink-bound gather leaves idle.
+  // ZPP_QWZ_PREFETCH_MODE=split instead gives K0 its own SMs (a budget of
+  // ZPP_QWZ_PREFETCH_SMS) and the gather the rest.
+  static const int pf_split = [] {
+    const char* e = getenv("ZPP_QWZ_PREFETCH_MODE");
+    return e && e[0] == 's' && e[1] == 'p';
+  }();
+  static const int gather_occ = [] {
+    const char* e = getenv("ZPP_QWZ_GATHER_OCC");
+    return e ? atoi(e) : 2;
+  }();
   const bool prefetch = next_shard && c->world > 1 && qwz_region(next_len, bits, block, ZPP_F64) == region;
   if (prefetch) {
     if (!c->side && (rc = check_cuda(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking), "side stream")))
@@ -442,13 +455,29 @@ int zpp_qwz_allgather_next(zpp_comm_t c, size_t sym_offset, const void* shard, i
     if (!c->ev_qbar && (rc = check_cuda(cudaEventCreateWithFlags(&c->ev_qbar, cudaEventDisableTiming), "event")))
       return rc;
     if ((rc = check_cuda(cudaEventRecord(c->ev_qbar, st), "record"))) return rc;
+  }
+  const void* codes[kMaxRanks];
+  const void* absmax[kMaxRanks];
+  for (int r = 0; r < c->world; ++r) {
+    codes[r] = c->peers[r] + base;
+    absmax[r] = c->peers[r] + base + abs_off;
+  }
+  {  // the gather is enqueued first, so its CTAs are placed first
+    SmBudget budget(prefetch && pf_split ? sm_count() - qwz_sms_for_prefetch(c->world) : 0);
+    OccCap cap(prefetch && !pf_split ? gather_occ : 0);
+    rc = launch_gather_dequant(codes, absmax, dtype == ZPP_F64 ? ZPP_F64 : ZPP_F32, c->world, c->rank, shard_len,
+                               bits, block, out, out_dtype, sec_out, sec_lo, sec_len, flag, st, out_stride);
+  }
+  if (rc) return rc;
+  if (prefetch) {
     if ((rc = check_cuda(cudaStreamWaitEvent(c->side, c->ev_qbar, 0), "wait"))) return rc;
     const size_t nbase = sym_offset + ((use + 1) & 1) * region;
     const size_t nabs = align256((size_t)code_bytes(next_len, bits, block));
     AddrSpec a;
     a.n = next_len;
     {
-      SmBudget budget(qwz_sms_for_prefetch(c->world));
+      SmBudget budget(pf_split ? qwz_sms_for_prefetch(c->world) : 0);
+      OccCap cap(pf_split ? 0 : 1);
       rc = launch_quantize(next_shard, dtype, a, next_len, bits, block, c->local + nbase, c->local + nbase + nabs, flag,
                            c->side);
     }
@@ -461,17 +490,6 @@ int zpp_qwz_allgather_next(zpp_comm_t c, size_t sym_offset, const void* shard, i
     c->pf_bits = bits;
     c->pf_block = block;
     c->pf_off = sym_offset;
-  }
-  const void* codes[kMaxRanks];
-  const void* absmax[kMaxRanks];
-  for (int r = 0; r < c->world; ++r) {
-    codes[r] = c->peers[r] + base;
-    absmax[r] = c->peers[r] + base + abs_off;
-  }
-  {
-    SmBudget budget(prefetch ? sm_count() - qwz_sms_for_prefetch(c->world) : 0);
-    rc = launch_gather_dequant(codes, absmax, dtype == ZPP_F64 ? ZPP_F64 : ZPP_F32, c->world, c->rank, shard_len,
-                               bits, block, out, out_dtype, sec_out, sec_lo, sec_len, flag, st, out_stride);
   }
   trace_mark(c, TR_GATHER, st);
   return rc;
@@ -631,7 +649,19 @@ int zpp_qgz_reduce_scatter_buckets(zpp_comm_t c, size_t sym_offset, const void* 
   // overlapping stages of one bucket (K2/K3 of a stage are short), a larger
   // share across buckets (K1 and the fold are both issue-bound; swept in
   // tools/qgz_xb_sweep.sh)
-  const int k1_sms = !pipelined ? 0
+  // ZPP_QGZ_XB_MODE=share: across buckets, K1(b+1) and K2/K3(b) both span
+  // every SM instead (K1 one CTA per SM, the fold ZPP_QGZ_K2_OCC = 2 CTAs
+  // per SM), sharing each SM's issue slots
+  static const int xb_share = [] {
+    const char* e = getenv("ZPP_QGZ_XB_MODE");
+    return e && e[0] == 's' && e[1] == 'h';
+  }();
+  static const int k2_occ_env = [] {
+    const char* e = getenv("ZPP_QGZ_K2_OCC");
+    return e ? atoi(e) : 2;
+  }();
+  const bool share = pipelined && stages == 1 && xb_share;
+  const int k1_sms = !pipelined || share ? 0
                      : stages > 1 ? (k1_sms_env > 0 ? k1_sms_env : sm_count() / 3)
                                   : (k1_xb_sms_env > 0 ? k1_xb_sms_env : sm_count() / 2);
   // Hop 1 either
@@ -662,6 +692,7 @@ int zpp_qgz_reduce_scatter_buckets(zpp_comm_t c, size_t sym_offset, const void* 
     return fail(ZPP_ERR_VALIDATION, "qgZ: the gradient buffer must be 16-byte aligned");
   auto k1 = [&](int u, cudaStream_t on) {
     SmBudget budget(u > 0 ? k1_sms : 0);  // K1(0) runs alone
+    OccCap cap(u > 0 && share ? 1 : 0);
     const int s = u % stages;
     const void* g = reinterpret_cast<const uint8_t*>(grad) + (size_t)(u / stages) * n * in_esz;
     AddrSpec a;
@@ -719,7 +750,8 @@ int zpp_qgz_reduce_scatter_buckets(zpp_comm_t c, size_t sym_offset, const void* 
       if ((rc = k1(s + 1, c->side))) return rc;
       if ((rc = check_cuda(cudaEventRecord(c->ev_k1, c->side), "record"))) return rc;
     }
-    SmBudget budget(pipelined && s + 1 < units ? sm_count() - k1_sms : 0);
+    SmBudget budget(pipelined && !share && s + 1 < units ? sm_count() - k1_sms : 0);
+    OccCap cap(share && s + 1 < units ? k2_occ_env : 0);
     // K2: the X messages for this rank, ascending local source -- pushed into
     // this rank's receive region by the group's K1s, or pulled from the peers
     const void* codes[kMaxRanks];

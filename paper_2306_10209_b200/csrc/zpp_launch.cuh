@@ -20,11 +20,26 @@ struct SmBudget {
 // SMs available to the next launch under the current budget
 inline int sm_budget() { return (t_sm_cap > 0 && t_sm_cap < sm_count()) ? t_sm_cap : sm_count(); }
 
+// Resident CTAs per SM for the next launches on this host thread (0 = the
+// kernel's occupancy).  Lets two stream-concurrent persistent grids share
+// every SM instead of splitting the SMs: the qwZ gather capped below its
+// occupancy leaves room for one CTA of the prefetched K0 on each SM.
+inline thread_local int t_occ_cap = 0;
+
+struct OccCap {
+  int saved;
+  explicit OccCap(int ctas) : saved(t_occ_cap) { t_occ_cap = ctas; }
+  ~OccCap() { t_occ_cap = saved; }
+};
+
+inline int occ_capped(int occ) { return (t_occ_cap > 0 && t_occ_cap < occ) ? t_occ_cap : (occ > 0 ? occ : 1); }
+
 // one resident wave of CTAs (persistent-style grid-stride), capped by work
 template <typename K>
 inline int grid_for(K kernel, int threads, int64_t needed_ctas) {
   int occ = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, 0) != cudaSuccess || occ <= 0) occ = 1;
+  occ = occ_capped(occ);
   int64_t g = (int64_t)sm_budget() * occ;
   if (needed_ctas < g) g = needed_ctas;
   return (int)(g < 1 ? 1 : g);

@@ -310,7 +310,7 @@ static int tma_grid(K k, const TmaTile& tt, int64_t tiles, size_t* smem) {
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*smem);
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 256, *smem);
-  return (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sm_budget() * std::max(occ, 1), tiles));
+  return (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sm_budget() * occ_capped(occ), tiles));
 }
 
 template <int IB, int OB, int NS, typename FO>

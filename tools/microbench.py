@@ -101,7 +101,10 @@ def fused_n1(lib, st, flag):
     for name, mk in (("randn*0.02", lambda: (torch.randn(M, device="cuda") * 0.02).half()),
                      ("synth", lambda: synth.device(1000, 0, M, torch.float16, "weight", device=torch.device("cuda")))):
         x = mk()
-        t = timeit(lambda: comm.qwz_allgather(x, out=out), iters=20, warm=5)
+        # ZPP_MB_WARM_S: keep the GPU busy on the same pass for that many
+        # seconds first (bench.py runs ~0.5 s of steps before its timed region)
+        warm = 5 + int(float(os.environ.get("ZPP_MB_WARM_S", "0")) / 1.1e-3)
+        t = timeit(lambda: comm.qwz_allgather(x, out=out), iters=20, warm=warm)
         report(f"fused N=1 qwZ pass, {name}", t, 5 * M + M // 2048 * 4)
         del x
         torch.cuda.empty_cache()
