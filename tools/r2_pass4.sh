@@ -3,6 +3,7 @@
 # ncu capture of rank 0 under peer traffic (2x2).
 O=${OUT:-gpurun_out/p4}; mkdir -p $O
 TR="python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1"
+timeout 900 python -m pytest tests/test_gpu_dist.py -q -x -k "four_gpus or qgz_hop1 or two_gpus" > $O/t4.log 2>&1; echo "tests rc=$?" >> $O/t4.log
 nvidia-smi nvlink -gt d -i 0 > $O/nvlink_gt_probe.txt 2>&1
 CUDA_VISIBLE_DEVICES=0 ZPP_MB_WARM_S=1.0 timeout 300 python tools/microbench.py fused > $O/fused_longwarm.txt 2>&1
 pf() {  # env...
