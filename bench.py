@@ -692,7 +692,7 @@ def step_leg(*, world, rank, dev, timed, steps, oversub, comm_cls, zpp, synth, s
     layer stack (h = 5120, 40 layers; zs/engine.py:345-398 order): forward qwZ
     (INT8/2048) layer by layer writing each layer's hpZ secondary, backward hpZ
     gathers inside the group in reverse layer order, gradient qgZ (INT4/512,
-    S = 2) per layer -- with and without the cross-layer prefetch of the next
+    S = 1, the measured optimum) per layer -- with and without the cross-layer prefetch of the next
     layer's quantization -- vs ZeRO-3's fp16 all-gather x2 + bf16
     reduce-scatter per layer (NCCL)."""
     import torch
@@ -704,7 +704,7 @@ def step_leg(*, world, rank, dev, timed, steps, oversub, comm_cls, zpp, synth, s
     layer_p = _pad(layer, world * 2048 * 4)
     shard = layer_p // world
     comm = comm_cls(group_size=X, qwz_shard=shard, hpz_sec=layer_p // X, hpz_layers=n_layers, qgz_elems=layer_p,
-                    qgz_stages=2, qgz_cfg=zpp.QuantConfig(bit_width=4, block_size=512))
+                    qgz_stages=1, qgz_cfg=zpp.QuantConfig(bit_width=4, block_size=512))
     ws = [synth.device(3000 + 100 * i + rank, 0, shard, torch.float16, "weight", device=dev) for i in range(n_layers)]
     g = synth.device(5000 + 1000 * rank, 0, layer_p, torch.bfloat16, "grad", device=dev)
     wout = torch.empty(layer_p, dtype=torch.float16, device=dev)
@@ -726,10 +726,10 @@ def step_leg(*, world, rank, dev, timed, steps, oversub, comm_cls, zpp, synth, s
     # after the last step: wout = layer 39 (forward), hout = layer 0 (backward)
     c1, b1 = sampled.qwz_check(wout, world, shard, seed_base=3000 + 100 * (n_layers - 1), samples=1024, rng_seed=rank)
     c2, b2 = sampled.qwz_check(hout, world, shard, seed_base=3000, samples=1024, rng_seed=rank + 7)
-    c3, b3 = sampled.qgz_check(gout, rank, world, X, layer_p, stages=2, seed_base=5000, samples=1024)
+    c3, b3 = sampled.qgz_check(gout, rank, world, X, layer_p, stages=1, seed_base=5000, samples=1024)
     add_parity("step_13b", c1 + c2 + c3, b1 + b2 + b3)
     comm.close()
-    res = {"workload": "fwd qwZ (prefetched) + bwd hpZ + grad qgZ (S=2) over 40 GPT-13B layers", "layers": n_layers,
+    res = {"workload": "fwd qwZ (prefetched) + bwd hpZ + grad qgZ (S=1) over 40 GPT-13B layers", "layers": n_layers,
            "layer_params": layer, "padded": layer_p, "groups": f"{world // X}x{X}",
            "zeropp_ms": t_pf * 1e3, "zeropp_no_prefetch_ms": t_no * 1e3, "prefetch_gain": t_no / t_pf}
     if world > 1 and not oversub:

@@ -34,6 +34,15 @@ struct OccCap {
 
 inline int occ_capped(int occ) { return (t_occ_cap > 0 && t_occ_cap < occ) ? t_occ_cap : (occ > 0 ? occ : 1); }
 
+// ZPP_BALANCED_GRID=0 turns the balanced grid-stride sizing off (A/B)
+inline bool balanced_grids() {
+  static const bool v = [] {
+    const char* e = getenv("ZPP_BALANCED_GRID");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+
 // one resident wave of CTAs (persistent-style grid-stride), capped by work
 template <typename K>
 inline int grid_for(K kernel, int threads, int64_t needed_ctas) {
@@ -41,7 +50,15 @@ inline int grid_for(K kernel, int threads, int64_t needed_ctas) {
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, 0) != cudaSuccess || occ <= 0) occ = 1;
   occ = occ_capped(occ);
   int64_t g = (int64_t)sm_budget() * occ;
-  if (needed_ctas < g) g = needed_ctas;
+  if (needed_ctas < g) {
+    g = needed_ctas;
+  } else if (balanced_grids()) {
+    // the same number of grid-stride rounds with every CTA doing every round:
+    // a small job (config 1: 1024 CTA-rounds over 296 slots) otherwise ends
+    // with a round at 46% of the GPU
+    const int64_t rounds = ceil_div(needed_ctas, g);
+    g = ceil_div(needed_ctas, rounds);
+  }
   return (int)(g < 1 ? 1 : g);
 }
 

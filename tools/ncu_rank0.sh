@@ -19,6 +19,11 @@ done
 RANK=0 LOCAL_RANK=0 timeout $T ncu --set full --clock-control none --import-source on \
   --metrics nvlrx__bytes.sum,nvltx__bytes.sum,dram__bytes_read.sum,dram__bytes_write.sum \
   -k regex:"dequant16_tma_kernel|drq_tma_kernel|dr_tma_kernel|quantize_push_kernel|drq_tbl_kernel|quantize_reg_kernel" \
-  --launch-skip ${SKIP:-8} --launch-count ${COUNT:-4} -o $O/nvl_n${N}_x${X} -f python tools/nvl_profile.py $X > $O/nvl_rank0.log 2>&1
+  --launch-skip ${SKIP:-8} --launch-count ${COUNT:-4} -o /tmp/nvl_n${N}_x${X} -f python tools/nvl_profile.py $X > $O/nvl_rank0.log 2>&1
 echo "rank0 rc=$?" >> $O/nvl_rank0.log
 wait
+# the report stays on the box (gpurun copies back at most 64 MiB): CSV pages only
+if [ -f /tmp/nvl_n${N}_x${X}.ncu-rep ]; then
+  ncu -i /tmp/nvl_n${N}_x${X}.ncu-rep --page raw --csv > $O/nvl_n${N}_x${X}_raw.csv 2>&1
+  ncu -i /tmp/nvl_n${N}_x${X}.ncu-rep --page details --csv > $O/nvl_n${N}_x${X}_details.csv 2>&1
+fi

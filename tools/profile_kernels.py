@@ -13,6 +13,8 @@ cases:
   k1       K1 swizzle-quantize of a 256 MiB bf16 bucket, INT4/512, 2x4 layout
   k2       K2 dequant->f64 fold->requant of 4 INT4/512 messages of 33.5M
   k3       K3 dequant->f64 fold of 2 INT4/512 (f64 absmax) segments -> fp32
+  c1q      config 1: quantize 16M fp32 -> INT8/2048
+  c1d      config 1: dequantize 16M INT8/2048 -> fp32
 """
 
 import json
@@ -94,6 +96,21 @@ def main():
             out = torch.empty(n, dtype=torch.float32, device=dev)
             fn = lambda: zpp.dequant_reduce(q64, torch.float32, out=out, flag=flag)  # noqa: E731
             alg = n_src * (n // 2 + n // 512 * 8) + 4 * n
+    elif case in ("c1q", "c1d"):
+        n = 1 << 24
+        x = torch.randn(n, generator=g, device=dev) * 0.02
+        codes = torch.empty(n, dtype=torch.uint8, device=dev)
+        am = torch.empty(n // 2048, dtype=torch.float32, device=dev)
+        y = torch.empty(n, dtype=torch.float32, device=dev)
+        q = lambda: lib.zpp_quantize(x.data_ptr(), _lib.F32, n, 8, 2048, codes.data_ptr(), am.data_ptr(),  # noqa: E731
+                                     flag.data_ptr(), st)
+        q()
+        if case == "c1q":
+            fn = q
+        else:
+            fn = lambda: lib.zpp_dequantize(codes.data_ptr(), am.data_ptr(), _lib.F32, n, 8, 2048,  # noqa: E731
+                                            y.data_ptr(), _lib.F32, flag.data_ptr(), st)
+        alg = 5 * n + n // 2048 * 4
     else:
         raise SystemExit(f"unknown case {case}")
     fn()

@@ -11,7 +11,7 @@ OUT=gpurun_out
 mkdir -p $OUT
 export CUDA_VISIBLE_DEVICES=0
 python bench.py --steps 2 --warmup 3 > $OUT/plain_$R.log 2>&1 || { echo "plain bench failed"; exit 1; }
-CASES="qwz1:quantize_reg_kernel gather4:dequant16_tma_kernel k0:quantize_reg_kernel k1:quantize_reg_kernel k2:drq_fast_kernel k3:dr_fast_kernel"
+CASES=${CASES:-"qwz1:quantize_reg_kernel gather4:dequant16_tma_kernel k0:quantize_reg_kernel k1:quantize_reg_kernel k2:drq_tbl_kernel k3:dr_fast_kernel c1q:quantize_reg_kernel c1d:dequant_wide_kernel"}
 for CK in $CASES; do
   C=${CK%%:*}
   python tools/profile_kernels.py $C 20 >> $OUT/kernels_$R.jsonl 2>> $OUT/kernels_$R.err || { echo "case $C failed"; exit 1; }
@@ -31,7 +31,8 @@ out = {}
 names = {"qwz1": "quantize_reg_kernel<deq> (fused qwZ self-gather)",
          "gather4": "dequant16_tma_kernel (gather over NVLink)",
          "k0": "quantize_reg_kernel", "k1": "quantize_reg_kernel<swizzle> (qgZ K1)",
-         "k2": "drq_fast_kernel", "k3": "dr_fast_kernel"}
+         "k2": "drq_tbl_kernel", "k3": "dr_fast_kernel", "c1q": "quantize_reg_kernel<fp32> (config 1)",
+         "c1d": "dequant_wide_kernel (config 1)"}
 scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 for f in glob.glob("/tmp/raw_*.csv"):
     c = os.path.basename(f)[4:-4]
@@ -45,6 +46,6 @@ for f in glob.glob("/tmp/raw_*.csv"):
             float(r[j].replace(",", "")) * scale.get(u[j], 1)
     except (ValueError, IndexError):
         pass
-json.dump(out, open("gpurun_out/ncu_traffic.json", "w"), indent=1)
+json.dump(out, open(os.environ.get("TRAFFIC_OUT", "gpurun_out/ncu_traffic.json"), "w"), indent=1)
 print(out)
 PY

@@ -23,3 +23,4 @@ TR="python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 
 OUT=$O bash tools/qgz_xb_sweep.sh
 timeout 900 $TR --master-port 29544 bench.py --gpus 4 > $O/b4.json 2> $O/b4.err; echo "rc=$?" >> $O/b4.err
 N=4 X=2 SKIP=10 COUNT=5 OUT=$O PORT=29571 NCU_TIMEOUT=420 bash tools/ncu_rank0.sh
+du -sh $O; find $O -size +8M -print -delete
