@@ -421,6 +421,13 @@ def run_ours(args):
         extra["qgz_stream_7b"] = stream_leg(comm_cls=Communicator, world=world, rank=rank, X=X, dev=dev, timed=timed,
                                             steps=args.steps, hbm_peak=hbm_peak, synth=synth, sampled=sampled,
                                             add_parity=add_parity, zpp=zpp)
+        if world >= 2 and X != world:
+            # the whole box as one group: buckets pipelined (K1 of bucket b+1
+            # beside the pull K2 of bucket b)
+            extra["qgz_stream_7b_one_group"] = stream_leg(
+                comm_cls=Communicator, world=world, rank=rank, X=world, dev=dev, timed=timed, steps=args.steps,
+                hbm_peak=hbm_peak, synth=synth, sampled=sampled, add_parity=add_parity, zpp=zpp,
+                parity_name="qgz_stream_one_group")
     if "step" in sections:
         extra["zeropp_step_13b"] = step_leg(world=world, rank=rank, dev=dev, timed=timed, steps=args.steps,
                                             oversub=oversub, comm_cls=Communicator, zpp=zpp, synth=synth,
@@ -640,7 +647,8 @@ def hpz_leg(*, comm_cls, world, dev, timed, oversub, nccl_allgather, synth, samp
     return res
 
 
-def stream_leg(*, comm_cls, world, rank, X, dev, timed, steps, hbm_peak, synth, sampled, add_parity, zpp):
+def stream_leg(*, comm_cls, world, rank, X, dev, timed, steps, hbm_peak, synth, sampled, add_parity, zpp,
+               parity_name="qgz_stream"):
     """BASELINE configs[3] as written: qgZ INT4/512 over a 7B-parameter bf16
     gradient stream -- 52 buckets of 256 MiB plus a 20,678,144-element tail
     zero-padded to W*S*512 (zs/engine.py:465-466) -- back to back through
@@ -667,7 +675,7 @@ def stream_leg(*, comm_cls, world, rank, X, dev, timed, steps, hbm_peak, synth, 
         chk, bad = chk + c, bad + m
     c, m = sampled.qgz_check(out[full * per:], rank, world, X, tail_pad, seed_base=2000 + full, samples=512,
                              valid=tail)
-    add_parity("qgz_stream", chk + c, bad + m)
+    add_parity(parity_name, chk + c, bad + m)
     comm.close()
     del grads, out
     torch.cuda.empty_cache()
@@ -677,6 +685,7 @@ def stream_leg(*, comm_cls, world, rank, X, dev, timed, steps, hbm_peak, synth, 
     t_roof = max(wire / (NVLINK_NOMINAL_GBS * 1e9), hbm / (hbm_peak * 1e9))
     return {"workload": "qgZ INT4/512 over a 7B bf16 gradient stream: 52 x 256 MiB buckets + padded tail",
             "params": n_total, "buckets": full, "tail": tail, "tail_padded": tail_pad, "groups": f"{world // X}x{X}",
+            "buckets_pipelined": world > 1 and X == world,
             "ms_per_step": t * 1e3, "effective_GBps": world * 2 * n_total / t / 1e9,
             "busbw_GBps": 2 * n_total * (world - 1) / world / t / 1e9 if world > 1 else None,
             "params_per_s": world * n_total / t,

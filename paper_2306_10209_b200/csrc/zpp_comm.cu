@@ -362,19 +362,19 @@ int zpp_qwz_allgather(zpp_comm_t c, size_t sym_offset, const void* shard, int dt
 // after this rank passed barrier(i).  The next call finds the prefetched
 // shard by (pointer, length, config, offset) and waits for it instead of
 // quantizing; any other shard waits for it and is quantized as usual.
-// SM budget of the prefetched K0: it must finish under the gather it hides
-// behind.  K0 moves ~3 HBM bytes per element at ~6.3 TB/s on the whole GPU;
-// the gather pulls (W-1) code bytes per element at ~640 GB/s, so K0 needs
-// about 0.3/(W-1) of the SMs; 0.4/(W-1) leaves margin (W = 2: 59 SMs,
-// W = 4: 20, W = 8: 8).  A fixed sm_count/6 made the prefetch slower than
-// the gather at W = 2 and the 40-layer step 14% slower than no prefetch.
+// SM budget of the prefetched K0 in split placement: it must finish under
+// the gather it hides behind without starving it.  K0 moves ~3 HBM bytes per
+// element at ~6.3 TB/s on the whole GPU; the gather pulls (W-1) code bytes
+// per element at ~640 GB/s, so K0 needs about 0.3/(W-1) of the SMs.  Swept
+// at W = 2 (profiles/r2/qwz_prefetch_sweep_n2_r2.jsonl): 20 SMs 19.5 ms,
+// 40 SMs 14.2, 59 SMs 15.7, 74 SMs 18.2 (no prefetch 14.6): 0.27 of the SMs.
 static int qwz_sms_for_prefetch(int world) {
   static const int v = [] {
     const char* e = getenv("ZPP_QWZ_PREFETCH_SMS");
     return e ? atoi(e) : 0;
   }();
   if (v > 0) return v;
-  const int s = (int)(sm_count() * 0.4 / std::max(1, world - 1) + 0.5);
+  const int s = (int)(sm_count() * 0.27 / std::max(1, world - 1) + 0.5);
   return std::min(std::max(8, s), sm_count() / 2);
 }
 
@@ -433,18 +433,24 @@ int zpp_qwz_allgather_next(zpp_comm_t c, size_t sym_offset, const void* shard, i
   trace_mark(c, TR_BARRIER, st);
   // prefetch: K0 of the next shard into the next call's half, on the side
   // stream, after this rank passed barrier(i); only for an unchanged layout.
-  // Default ("share"): both grids span every SM -- the gather capped at
-  // ZPP_QWZ_GATHER_OCC (2) CTAs per SM, which leaves room for one CTA of K0
-  // per SM, so K0 runs in the issue slots the NVLink-bound gather leaves idle.
-  // ZPP_QWZ_PREFETCH_MODE=split instead gives K0 its own SMs (a budget of
-  // ZPP_QWZ_PREFETCH_SMS) and the gather the rest.
-  static const int pf_split = [] {
+  // Two placements (40-layer GPT-13B forward, profiles/r2/qwz_prefetch_sweep*):
+  //  * share (W >= 3): both grids span every SM, the gather capped at
+  //    ZPP_QWZ_GATHER_OCC = 3 CTAs per SM (of 4) and K0 at one CTA per SM, so
+  //    K0 runs in the issue slots the NVLink-bound gather leaves idle.  W = 4:
+  //    16.1 ms vs 17.6 ms without prefetch (occupancy 2: 18.4; 1: 30.3;
+  //    split with 20 SMs: 16.3);
+  //  * split (W = 2): K0 on its own ZPP_QWZ_PREFETCH_SMS = 40 SMs, the gather
+  //    on the rest: 14.2 ms vs 14.6 ms (share at occupancy 2: 18.2 -- the
+  //    W = 2 gather needs its full occupancy).
+  // ZPP_QWZ_PREFETCH_MODE=share|split overrides.
+  static const int pf_mode_env = [] {
     const char* e = getenv("ZPP_QWZ_PREFETCH_MODE");
-    return e && e[0] == 's' && e[1] == 'p';
+    return !e ? 0 : (e[0] == 's' && e[1] == 'p') ? 2 : 1;  // 1 share, 2 split
   }();
+  const bool pf_split = pf_mode_env == 2 || (pf_mode_env == 0 && c->world == 2);
   static const int gather_occ = [] {
     const char* e = getenv("ZPP_QWZ_GATHER_OCC");
-    return e ? atoi(e) : 2;
+    return e ? atoi(e) : 3;
   }();
   const bool prefetch = next_shard && c->world > 1 && qwz_region(next_len, bits, block, ZPP_F64) == region;
   if (prefetch) {
@@ -613,7 +619,14 @@ int zpp_qgz_reduce_scatter_buckets(zpp_comm_t c, size_t sym_offset, const void* 
     return e ? atoi(e) : 1;
   }();
   const int units = n_buckets * stages;
-  const bool pipelined = stages > 1 || (n_buckets > 1 && xb_env != 0);
+  // Bucket pipelining pays only when hop 2 is a self-send (Y = 1, pull K2):
+  // 8 x 256 MiB buckets (profiles/r2/qgz_bucket_pipeline_sweep_r2.jsonl),
+  // 1x4: 145.6 us per bucket vs 171.9 back to back; 1x2: 175.5 vs 182.7.
+  // With a second hop (push K1 + K2 + cross barrier + K3) every split lost
+  // (2x2: 216-273 vs 210.6), so those buckets run back to back.
+  // ZPP_QGZ_XB=0 disables it, ZPP_QGZ_XB=2 forces it (A/B).
+  const bool xb = n_buckets > 1 && (xb_env == 2 || (xb_env == 1 && Y == 1));
+  const bool pipelined = stages > 1 || xb;
   if (pipelined && !c->ev_start) {
     if (!c->side) rc = check_cuda(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking), "side stream");
     if (!rc) rc = check_cuda(cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming), "event");
@@ -663,7 +676,7 @@ int zpp_qgz_reduce_scatter_buckets(zpp_comm_t c, size_t sym_offset, const void* 
   const bool share = pipelined && stages == 1 && xb_share;
   const int k1_sms = !pipelined || share ? 0
                      : stages > 1 ? (k1_sms_env > 0 ? k1_sms_env : sm_count() / 3)
-                                  : (k1_xb_sms_env > 0 ? k1_xb_sms_env : sm_count() / 2);
+                                  : (k1_xb_sms_env > 0 ? k1_xb_sms_env : (X >= 4 ? sm_count() / 2 : sm_count() * 2 / 5));
   // Hop 1 either
   //  * push: K1 (quantize_push_kernel) streams each message into the receiving
   //    peer's [src_loc][c][e] region with TMA bulk stores while it quantizes,

@@ -40,6 +40,14 @@ def test_two_gpus(group):
     _run(2, group, 2)
 
 
+def test_two_gpus_bucket_pipeline_forced():
+    """2x1 (a second hop) with the bucket pipelining forced on (ZPP_QGZ_XB=2;
+    by default only one-group layouts pipeline buckets) and the qwZ prefetch
+    in share placement: the stream and layer cases of dist_worker stay
+    bit-exact on the code paths the defaults skip at this shape."""
+    _run(2, 1, 2, env={"ZPP_QGZ_XB": "2", "ZPP_QWZ_PREFETCH_MODE": "share"})
+
+
 def test_four_gpus_2x2():
     if torch.cuda.device_count() < 4:
         pytest.skip("needs 4 GPUs")
