@@ -280,6 +280,18 @@ static int run_gather(const SrcTable& t, int n_src, int rot, int64_t shard_len, 
       return check_cuda(cudaGetLastError(), "dequant16_kernel launch");
     }
   }
+  if constexpr (BITS == 8 && std::is_same<O, float>::value && std::is_same<A, float>::value) {
+    // INT8 -> fp32 (config 1): 4-element groups, warp-contiguous stores
+    bool ok = aligned16(out) && sec_out == nullptr && shard_len % 4 == 0 && (out_stride % 4 == 0);
+    for (int i = 0; i < n_src; ++i) ok = ok && (reinterpret_cast<uintptr_t>(t.codes[i]) & 3) == 0;
+    if (ok) {
+      auto k = dequant8_f32_kernel<8>;
+      const int grid = grid_for(k, 256, ceil_div(shard_len / 4, 256 * 4));
+      k<<<grid, 256, 0, st>>>(t, n_src, shard_len, block, reinterpret_cast<float*>(out),
+                              out_stride ? out_stride : shard_len, flag);
+      return check_cuda(cudaGetLastError(), "dequant8_f32_kernel launch");
+    }
+  }
   if constexpr (sizeof(O) >= 4 && std::is_same<A, float>::value) {
     // fp32 / f64 outputs, whole 16-byte code units, no write-through
     constexpr int64_t E = 128 / BITS;

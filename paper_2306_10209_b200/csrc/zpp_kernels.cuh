@@ -522,7 +522,11 @@ quantize_reg_kernel(const T* __restrict__ x, Addr addr, int64_t n_blocks, uint8_
   // byte) keeps the single buffer: the pipelined version's 116 registers halve
   // occupancy and measured 68 -> 74 us (16 lanes x 32 elements, 78
   // registers: 78 us).
-  constexpr bool PIPE = !DEQ && BITS == 8;
+  // The pipeline keeps two input buffers live: only when one buffer is at
+  // most 32 registers (fp16/bf16 x 64, fp32 x 32).  fp32 x 64 (config 1's
+  // INT8/2048 blocks) pipelined took 170 registers, one CTA per SM and 45% of
+  // the DRAM peak.
+  constexpr bool PIPE = !DEQ && BITS == 8 && sizeof(T) * EPL <= 128;
   if constexpr (!PIPE) {
     for (int64_t wb = gwarp * TPW; wb < n_blocks; wb += nwarp * TPW) {
       const int64_t b = wb + team;
@@ -877,6 +881,60 @@ dequant16_kernel(SrcTable src, int n_src, int rot, int64_t shard_len, int64_t B,
           for (int i = 0; i < E; ++i)
             if (i < cnt && k0 + i >= 0 && k0 + i < sec_len) store_scalar<O>(sec_out + k0, i, h[i / 2] >> (16 * (i & 1)));
         }
+      }
+    }
+  }
+  if (bad) raise_flag(flag, FLAG_BADCODE);
+}
+
+// ---------------------------------------------------------------------------
+// K4, INT8 codes -> fp32 (config 1's dequantize): the same arithmetic as
+// dequant_wide_kernel, but a lane owns one 4-element group (one 32-bit code
+// word, one float4 of output) per step, consecutive lanes consecutive groups:
+// every warp-wide store writes 512 contiguous bytes.  (With 16-element units
+// a lane's four float4 stores sit 64 B apart from its neighbours', so each
+// store instruction half-fills 32-byte sectors: 26 us for 16M elements, DRAM
+// at 15% of peak, 77% of cycles with no eligible warp.)  Four groups per lane
+// are loaded before any is converted, to keep loads in flight.
+// Requires shard_len % 4 == 0 and 16-byte aligned output rows.
+template <int BITS = 8>  // a template: the header is compiled into several translation units
+__global__ void __launch_bounds__(256)
+dequant8_f32_kernel(SrcTable src, int n_src, int64_t shard_len, int64_t B, float* __restrict__ out,
+                    int64_t out_stride, uint32_t* __restrict__ flag) {
+  if (comm_aborted(flag)) return;
+  const int64_t groups = shard_len >> 2;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const bool pow2 = (B & (B - 1)) == 0;
+  const int lg = pow2 ? __ffsll(B) - 1 : 0;
+  bool bad = false;
+  for (int s = 0; s < n_src; ++s) {
+    const uint32_t* cs = reinterpret_cast<const uint32_t*>(src.codes[s]);
+    const float* am = reinterpret_cast<const float*>(src.absmax[s]);
+    float4* o = reinterpret_cast<float4*>(out + (int64_t)s * out_stride);
+    for (int64_t g0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g0 < groups; g0 += 4 * stride) {
+      uint32_t w[4];
+      float a[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int64_t g = g0 + i * stride;
+        const bool ok = g < groups;
+        w[i] = ok ? __ldg(cs + g) : 0u;
+        const int64_t e0 = g << 2;
+        a[i] = ok ? __ldg(am + (pow2 ? (e0 >> lg) : e0 / B)) : 0.0f;
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int64_t g = g0 + i * stride;
+        if (g >= groups) break;
+        bad |= has_byte_0x80(w[i]);
+        const double sc = scale_of<8>((double)a[i]);
+        const uint32_t b = w[i] ^ 0x80808080u;
+        float v[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          v[j] = __double2float_rn(
+              __dmul_rn(__dsub_rn(__hiloint2double(0x43380000, (int)__byte_perm(b, 0, 0x4440 + j)), Bias<8>::kD), sc));
+        o[g] = make_float4(v[0], v[1], v[2], v[3]);
       }
     }
   }
