@@ -1712,7 +1712,7 @@ template <int OBITS, typename FO>
 __device__ __forceinline__ void drq_epilogue(const double (&acc)[16], int64_t b, int tl, int64_t e0, bool active,
                                              int64_t u, uint8_t* __restrict__ codes, double* __restrict__ absmax,
                                              uint32_t* __restrict__ flag, FO* __restrict__ final_out,
-                                             float* fo_tbl = nullptr) {
+                                             float* fo_tbl = nullptr, bool span = false) {
   constexpr int QMAX = Codes<OBITS>::kQmax;
   double mx = absmax16(acc);
 #pragma unroll
@@ -1756,9 +1756,16 @@ __device__ __forceinline__ void drq_epilogue(const double (&acc)[16], int64_t b,
         const uint32_t a = base + (uint32_t)(__double2loint(r[i]) * 4);
         asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v[i]) : "r"(a) : "memory");
       }
-      float* dst = reinterpret_cast<float*>(final_out) + e0;
+      if (span) {  // coalesced layout (store_span_f32): the block's 512 outputs are contiguous
+        float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(final_out) + b * 512);
 #pragma unroll
-      for (int i = 0; i < 4; ++i) reinterpret_cast<float4*>(dst)[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+        for (int k = 0; k < 4; ++k) dst[k * 32 + tl] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+      } else {
+        float* dst = reinterpret_cast<float*>(final_out) + e0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          reinterpret_cast<float4*>(dst)[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+      }
     }
   } else if (active) {
     // hop 2 to itself: K3's fold of one source, RN(+0.0 + RN(code*s2)) = RN(code*s2)
@@ -1960,6 +1967,34 @@ __device__ __forceinline__ double lds_f64(uint32_t addr) {
   return v;
 }
 
+// Warp-coalesced fp32 output for K3 (and any fold whose warp covers 512
+// contiguous elements, 32 units of 16): instead of lane l folding elements
+// 16l..16l+15 and storing four float4s 64 B apart from its neighbours' (each
+// store instruction then half-fills every 32-byte sector it touches: ncu on
+// K3 showed the L1/L2 store path 70% busy at 14% of the DRAM peak), lane l
+// folds elements k*128 + 4l .. +3 for k = 0..3, whose codes are four 16-bit
+// pieces at byte k*64 + 2l of the warp's 256-byte INT4 span, and store k of
+// the warp writes 512 contiguous bytes.  The 16 nibbles are packed in that
+// order, so acc[4k + e] is element k*128 + 4l + e.  Arithmetic per element is
+// unchanged.
+__device__ __forceinline__ uint2 int4_span_pieces_g(const uint8_t* __restrict__ span, int lane) {
+  const uint16_t* p = reinterpret_cast<const uint16_t*>(span) + lane;
+  const uint32_t p0 = __ldg(p), p1 = __ldg(p + 32), p2 = __ldg(p + 64), p3 = __ldg(p + 96);
+  return make_uint2(p0 | (p1 << 16), p2 | (p3 << 16));
+}
+__device__ __forceinline__ uint2 int4_span_pieces_s(const uint8_t* span, int lane) {
+  const uint16_t* p = reinterpret_cast<const uint16_t*>(span) + lane;
+  const uint32_t p0 = p[0], p1 = p[32], p2 = p[64], p3 = p[96];
+  return make_uint2(p0 | (p1 << 16), p2 | (p3 << 16));
+}
+__device__ __forceinline__ void store_span_f32(float* __restrict__ span, const double (&acc)[16], int lane) {
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    reinterpret_cast<float4*>(span)[k * 32 + lane] =
+        make_float4(from_f64<float>(acc[4 * k]), from_f64<float>(acc[4 * k + 1]), from_f64<float>(acc[4 * k + 2]),
+                    from_f64<float>(acc[4 * k + 3]));
+}
+
 // acc[i] (+)= T[code_i + 8] for the 16 INT4 codes in w (element order as
 // fold16); `slot` = shared address of the source's table (256-byte aligned)
 template <bool ASSIGN>
@@ -2005,12 +2040,18 @@ drq_tbl_kernel(SrcTable src, int64_t n, int lg1, int64_t n_blocks_out, uint8_t* 
   bool bad = false;
   uint2 w[NSRC], wn[NSRC];
   float m[NSRC], mn[NSRC];
+  // final fp32 output and whole blocks: coalesced layout (store_span_f32);
+  // the fp32 table path of drq_epilogue is the only consumer, codes outputs
+  // keep the per-lane order their packing needs
+  const bool span = std::is_same<FO, float>::value && OBITS == 4 && (n & 511) == 0;
   auto load = [&](int64_t b, uint2 (&wv)[NSRC], float (&mv)[NSRC]) {
     const int64_t e0 = b * 512 + (int64_t)tl * 16;
     const bool blk = b < n_blocks_out, ok = blk && e0 < n;
 #pragma unroll
     for (int j = 0; j < NSRC; ++j) {
-      wv[j] = ok ? __ldg(reinterpret_cast<const uint2*>(src.codes[j]) + (e0 >> 4)) : make_uint2(0, 0);
+      wv[j] = !ok ? make_uint2(0, 0)
+              : span ? int4_span_pieces_g(src.codes[j] + b * 256, tl)
+                     : __ldg(reinterpret_cast<const uint2*>(src.codes[j]) + (e0 >> 4));
       mv[j] = blk ? __ldg(reinterpret_cast<const float*>(src.absmax[j]) + ((b * 512) >> lg1)) : 0.0f;
     }
   };
@@ -2042,7 +2083,8 @@ drq_tbl_kernel(SrcTable src, int64_t n, int lg1, int64_t n_blocks_out, uint8_t* 
       if (j < NT) fold16_tbl4<false>(w[j], slot0 + j * 256, acc, bad);
       else fold16<4, true>(w[j], div_q_f32<7>(m[j]), acc, bad);
     }
-    drq_epilogue<OBITS, FO>(acc, b, tl, e0, active, u, codes, absmax, flag, final_out, fo_all[threadIdx.x >> 5]);
+    drq_epilogue<OBITS, FO>(acc, b, tl, e0, active, u, codes, absmax, flag, final_out, fo_all[threadIdx.x >> 5],
+                            span);
   }
   if (bad) raise_flag(flag, FLAG_BADCODE);
 }
@@ -2067,11 +2109,24 @@ dr_fast_kernel(SrcTable src, int64_t n, int lg, O* __restrict__ out, double post
   bool bad = false;
   V w[NSRC], wn[NSRC];
   A m[NSRC], mn[NSRC];
+  // TBL with fp32 output and whole 512-element warp spans: coalesced layout
+  // (see store_span_f32); warp-uniform
+  constexpr bool CAN_SPAN = TBL && sizeof(O) == 4;
+  const bool span = CAN_SPAN && (n & 511) == 0;
+  const int lane = threadIdx.x & 31;
   auto load = [&](int64_t u, V (&wv)[NSRC], A (&mv)[NSRC]) {
     const int64_t ua = TBL ? (u & ~int64_t(31)) : u;
 #pragma unroll
     for (int j = 0; j < NSRC; ++j) {
-      wv[j] = u < units ? __ldg(reinterpret_cast<const V*>(src.codes[j]) + u) : V{};
+      if constexpr (CAN_SPAN) {
+        if (span) {
+          wv[j] = u < units ? int4_span_pieces_g(src.codes[j] + ua * 8, lane) : V{};
+        } else {
+          wv[j] = u < units ? __ldg(reinterpret_cast<const V*>(src.codes[j]) + u) : V{};
+        }
+      } else {
+        wv[j] = u < units ? __ldg(reinterpret_cast<const V*>(src.codes[j]) + u) : V{};
+      }
       mv[j] = ua < units ? __ldg(reinterpret_cast<const A*>(src.absmax[j]) + ((ua * 16) >> lg)) : A(0);
     }
   };
@@ -2106,6 +2161,12 @@ dr_fast_kernel(SrcTable src, int64_t n, int lg, O* __restrict__ out, double post
       for (int i = 0; i < 16; ++i) acc[i] = __dmul_rn(acc[i], post_scale);
     }
     O* dst = out + u * 16;
+    if constexpr (CAN_SPAN) {
+      if (span) {
+        store_span_f32(reinterpret_cast<float*>(out + (u & ~int64_t(31)) * 16), acc, lane);
+        continue;
+      }
+    }
     if constexpr (sizeof(O) == 4) {
 #pragma unroll
       for (int i = 0; i < 4; ++i)
@@ -2176,7 +2237,7 @@ __device__ __forceinline__ double tma_absmax(const SrcTable& src, int j, const u
 
 // K2 (hop-1 fold + requant into 512-element blocks, or the final partition
 // when hop 2 is a self-send): fp32 absmax sources, warp = output block.
-template <int IBITS, int OBITS, int NSRC, typename FO, int STAGES, bool TBL = false>
+template <int IBITS, int OBITS, int NSRC, typename FO, int STAGES, bool TBL = false, bool SPAN = false>
 __global__ void __launch_bounds__(256)
 drq_tma_kernel(SrcTable src, int64_t n, TmaTile tt, uint8_t* __restrict__ codes, double* __restrict__ absmax,
                uint32_t* __restrict__ flag, FO* __restrict__ final_out) {
@@ -2209,6 +2270,11 @@ drq_tma_kernel(SrcTable src, int64_t n, TmaTile tt, uint8_t* __restrict__ codes,
                                            &full[k]);
   }
   bool bad = false;
+  // final fp32 output through the product tables, whole blocks: coalesced
+  // layout (store_span_f32); a template choice (the host checks n % 512 == 0)
+  // because a runtime switch took the kernel from 80 to 124 registers
+  static_assert(!SPAN || (TBL && std::is_same<FO, float>::value && OBITS == 4), "span layout: fp32 table path only");
+  constexpr bool span = SPAN;
   int k = 0;
   for (int64_t t = blockIdx.x; t < tiles; t += G, ++k) {
     const int slot = k % STAGES;
@@ -2240,7 +2306,9 @@ drq_tma_kernel(SrcTable src, int64_t n, TmaTile tt, uint8_t* __restrict__ codes,
 #pragma unroll
         for (int j = 0; j < NSRC; ++j) {
           const uint8_t* sl = stage + j * (tt.code_slot + tt.abs_slot);
-          const uint2 w = active ? *reinterpret_cast<const uint2*>(sl + lu * UB) : make_uint2(0, 0);
+          const uint2 w = !active ? make_uint2(0, 0)
+                          : span ? int4_span_pieces_s(sl + (lu & ~31) * UB, tl)
+                                 : *reinterpret_cast<const uint2*>(sl + lu * UB);
           if (j == 0) fold16_tbl4<true>(w, slot0, acc, bad);
           else fold16_tbl4<false>(w, slot0 + j * 256, acc, bad);
         }
@@ -2260,7 +2328,7 @@ drq_tma_kernel(SrcTable src, int64_t n, TmaTile tt, uint8_t* __restrict__ codes,
         for (int i = 0; i < 16; ++i) acc[i] = 0.0;  // zero padding of a partial last block
       }
       drq_epilogue<OBITS, FO>(acc, (u0 + ob * 32) / 32, tl, unit * 16, active, unit, codes, absmax, flag, final_out,
-                              TBL ? fo_all[wid] : nullptr);
+                              TBL ? fo_all[wid] : nullptr, span);
     }
     __syncthreads();  // every thread is done with this slot before it is refilled
   }
@@ -2268,7 +2336,7 @@ drq_tma_kernel(SrcTable src, int64_t n, TmaTile tt, uint8_t* __restrict__ codes,
 }
 
 // K3 (hop-2 fold into the rank's partition): f64 absmax sources from K2.
-template <int BITS, int NSRC, typename O, int STAGES, bool TBL = false>
+template <int BITS, int NSRC, typename O, int STAGES, bool TBL = false, bool SPAN = false>
 __global__ void __launch_bounds__(256)
 dr_tma_kernel(SrcTable src, int64_t n, TmaTile tt, O* __restrict__ out, uint32_t* __restrict__ flag) {
   if (comm_aborted(flag)) return;
@@ -2298,6 +2366,10 @@ dr_tma_kernel(SrcTable src, int64_t n, TmaTile tt, O* __restrict__ out, uint32_t
                                            &full[k]);
   }
   bool bad = false;
+  // TBL with fp32 output and whole 512-element warp spans: coalesced layout
+  // (a template choice; the host checks n % 512 == 0)
+  static_assert(!SPAN || (TBL && sizeof(O) == 4), "span layout: fp32 table path only");
+  constexpr bool span = SPAN;
   int k = 0;
   for (int64_t t = blockIdx.x; t < tiles; t += G, ++k) {
     const int slot = k % STAGES;
@@ -2328,9 +2400,17 @@ dr_tma_kernel(SrcTable src, int64_t n, TmaTile tt, O* __restrict__ out, uint32_t
         if (unit >= units) continue;  // past the end (the warp's last loop trip)
 #pragma unroll
         for (int j = 0; j < NSRC; ++j) {
-          const uint2 w = *reinterpret_cast<const uint2*>(stage + j * (tt.code_slot + tt.abs_slot) + lu * UB);
+          const uint8_t* sj = stage + j * (tt.code_slot + tt.abs_slot);
+          const uint2 w = span ? int4_span_pieces_s(sj + (lu & ~31) * UB, tid & 31)
+                               : *reinterpret_cast<const uint2*>(sj + lu * UB);
           if (j == 0) fold16_tbl4<true>(w, slot0, acc, bad);
           else fold16_tbl4<false>(w, slot0 + j * 256, acc, bad);
+        }
+        if constexpr (sizeof(O) == 4) {
+          if (span) {  // coalesced layout, see store_span_f32
+            store_span_f32(reinterpret_cast<float*>(out + (u0 + (lu & ~31)) * 16), acc, tid & 31);
+            continue;
+          }
         }
       } else {
         if (unit >= units) break;

@@ -110,6 +110,16 @@ static bool drq_fast_ok(int n_src, int64_t n, int64_t in_block, int64_t out_bloc
          (in_block & (in_block - 1)) == 0 && (n_src == 1 || n_src == 2 || n_src == 4 || n_src == 8);
 }
 
+// ZPP_NO_SPAN=1 (development A/B only): fp32 outputs of the INT4 folds in the
+// per-lane layout instead of the warp-coalesced span layout
+static bool span_on() {
+  static const bool v = [] {
+    const char* e = getenv("ZPP_NO_SPAN");
+    return !(e && e[0] == '1');
+  }();
+  return v;
+}
+
 // ZPP_NO_TBL=1 (development A/B only): INT4 folds without product tables
 bool tbl_off() {
   static const bool off = [] {
@@ -318,8 +328,11 @@ static int run_drq_tma(const SrcTable& t, int64_t n, int64_t in_block, uint8_t* 
                        uint32_t* flag, cudaStream_t st) {
   const TmaTile tt = tma_tile(NS, IB, in_block, sizeof(float));
   // INT4 sources with one scale per warp tile: product tables
-  auto k = (IB == 4 && in_block % 512 == 0 && !tbl_off()) ? drq_tma_kernel<IB, OB, NS, FO, kTmaStages, IB == 4>
-                                                          : drq_tma_kernel<IB, OB, NS, FO, kTmaStages, false>;
+  constexpr bool can_span = IB == 4 && OB == 4 && std::is_same<FO, float>::value;
+  const bool tbl = IB == 4 && in_block % 512 == 0 && !tbl_off();
+  auto k = tbl ? (can_span && n % 512 == 0 && span_on() ? drq_tma_kernel<IB, OB, NS, FO, kTmaStages, IB == 4, can_span>
+                                                       : drq_tma_kernel<IB, OB, NS, FO, kTmaStages, IB == 4>)
+               : drq_tma_kernel<IB, OB, NS, FO, kTmaStages, false>;
   size_t smem = 0;
   const int grid = tma_grid(k, tt, ceil_div(n / 16, tt.tu), &smem);
   k<<<grid, 256, smem, st>>>(t, n, tt, codes, absmax, flag, fo);
@@ -372,8 +385,11 @@ int launch_drq_tma(const void* const* codes, const void* const* absmax, int n_sr
 template <int B, int NS, typename O>
 static int run_dr_tma(const SrcTable& t, int64_t n, int64_t block, O* out, uint32_t* flag, cudaStream_t st) {
   const TmaTile tt = tma_tile(NS, B, block, sizeof(double));
-  auto k = (B == 4 && block % 512 == 0 && !tbl_off()) ? dr_tma_kernel<B, NS, O, kTmaStages, B == 4>
-                                                      : dr_tma_kernel<B, NS, O, kTmaStages, false>;
+  constexpr bool can_span = B == 4 && sizeof(O) == 4;
+  const bool tbl = B == 4 && block % 512 == 0 && !tbl_off();
+  auto k = tbl ? (can_span && n % 512 == 0 && span_on() ? dr_tma_kernel<B, NS, O, kTmaStages, B == 4, can_span>
+                                                       : dr_tma_kernel<B, NS, O, kTmaStages, B == 4>)
+               : dr_tma_kernel<B, NS, O, kTmaStages, false>;
   size_t smem = 0;
   const int grid = tma_grid(k, tt, ceil_div(n / 16, tt.tu), &smem);
   k<<<grid, 256, smem, st>>>(t, n, tt, out, flag);
