@@ -85,7 +85,12 @@ def load():
                     f"libzpp.so not found at {LIB_PATH}; build it with "
                     "`python -c 'import __graft_entry__ as g; g.build()'`")
             lib = ctypes.CDLL(LIB_PATH)
+            # ZPP_LIB (development A/B against an older build) may lack newer
+            # entries; the in-tree library must export every one
+            alt = "ZPP_LIB" in os.environ
             for name, (res, args) in SIGNATURES.items():
+                if alt and not hasattr(lib, name):
+                    continue
                 fn = getattr(lib, name)
                 fn.restype = res
                 fn.argtypes = args

@@ -77,6 +77,20 @@ __device__ __forceinline__ double dmax_nn(double mx, double a) { return a > mx ?
 // magnitude is taken once at the end.  A sequential chain: a pairwise tree
 // keeps 8 more doubles live and took K2 from 80 to 104 registers.  NaNs lose
 // every comparison (kept only in slot 0); the callers test !(mx <= DBL_MAX).
+// Warp-wide max of non-negative doubles (or NaN/inf) in two redux.sync
+// integer reductions: a non-negative double's bit pattern orders like its
+// value, so the max has the largest high word and, among the lanes holding
+// that high word, the largest low word.  Replaces five shuffle + DSETP +
+// 2 select levels (25 instructions per lane).  NaN high words (0x7FF8...)
+// exceed every finite and infinite one, so a NaN anywhere gives NaN, which the
+// callers' !(mx <= DBL_MAX) test flags.
+__device__ __forceinline__ double warp_max_nonneg(double x) {
+  const unsigned hi = (unsigned)__double2hiint(x), lo = (unsigned)__double2loint(x);
+  const unsigned H = __reduce_max_sync(0xffffffffu, hi);
+  const unsigned L = __reduce_max_sync(0xffffffffu, hi == H ? lo : 0u);
+  return __hiloint2double((int)H, (int)L);
+}
+
 __device__ __forceinline__ double absmax16(const double (&a)[16]) {
   double m = a[0];
 #pragma unroll

@@ -1715,8 +1715,7 @@ __device__ __forceinline__ void drq_epilogue(const double (&acc)[16], int64_t b,
                                              float* fo_tbl = nullptr, bool span = false) {
   constexpr int QMAX = Codes<OBITS>::kQmax;
   double mx = absmax16(acc);
-#pragma unroll
-  for (int off = 16; off >= 1; off >>= 1) mx = dmax_nn(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+  mx = warp_max_nonneg(mx);
   if (tl == 0) {
     absmax[b] = mx;
     if (!(mx <= DBL_MAX)) raise_flag(flag, FLAG_NONFINITE);

@@ -16,7 +16,9 @@ for CK in $CASES; do
   C=${CK%%:*}
   python tools/profile_kernels.py $C 20 >> $OUT/kernels_$R.jsonl 2>> $OUT/kernels_$R.err || { echo "case $C failed"; exit 1; }
 done
+# our kernels only (the synthetic-input generation is torch elementwise work)
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $OUT/ncu_launches_$R.csv \
+    -k regex:"quantize_|dequant|drq_|dr_fast|dr_tma|gather_copy|barrier_kernel|wire_|scales_kernel" \
     python bench.py --steps 2 --warmup 3 > $OUT/ncu_launches_$R.log 2>&1
 for CK in $CASES; do
   C=${CK%%:*}; K=${CK##*:}
