@@ -623,9 +623,11 @@ int zpp_qgz_reduce_scatter_buckets(zpp_comm_t c, size_t sym_offset, const void* 
   // 8 x 256 MiB buckets (profiles/r2/qgz_bucket_pipeline_sweep_r2.jsonl),
   // 1x4: 145.6 us per bucket vs 171.9 back to back; 1x2: 175.5 vs 182.7.
   // With a second hop (push K1 + K2 + cross barrier + K3) every split lost
-  // (2x2: 216-273 vs 210.6), so those buckets run back to back.
+  // (2x2: 216-273 vs 210.6), so those buckets run back to back, and so do
+  // the buckets of a 1-GPU world (no NVLink wait to hide: 7B stream 15.7 vs
+  // 11.6 ms).
   // ZPP_QGZ_XB=0 disables it, ZPP_QGZ_XB=2 forces it (A/B).
-  const bool xb = n_buckets > 1 && (xb_env == 2 || (xb_env == 1 && Y == 1));
+  const bool xb = n_buckets > 1 && (xb_env == 2 || (xb_env == 1 && Y == 1 && X > 1));
   const bool pipelined = stages > 1 || xb;
   if (pipelined && !c->ev_start) {
     if (!c->side) rc = check_cuda(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking), "side stream");
