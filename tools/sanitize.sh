@@ -15,6 +15,9 @@ ZPP_FORCE_TMA=1 timeout 1200 $CS python -m pytest -q -x -p no:cacheprovider test
 echo "rc=$?" >> $O/${TOOL}_single.log
 timeout 900 $CS python -m pytest -q -x -p no:cacheprovider tests/test_gpu_comm_single.py > $O/${TOOL}_comm1.log 2>&1
 echo "rc=$?" >> $O/${TOOL}_comm1.log
+timeout 900 $CS python -m pytest -q -x -p no:cacheprovider tests/test_gpu_collectives.py -k "qwz_golden" \
+  > $O/${TOOL}_gather.log 2>&1
+echo "rc=$?" >> $O/${TOOL}_gather.log
 export WORLD_SIZE=2 MASTER_ADDR=127.0.0.1
 for mode in pull push; do
   export MASTER_PORT=$((29600 + RANDOM % 300)) ZPP_QGZ_MODE=$mode
