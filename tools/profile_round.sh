@@ -11,7 +11,7 @@ OUT=gpurun_out
 mkdir -p $OUT
 export CUDA_VISIBLE_DEVICES=0
 python bench.py --steps 2 --warmup 3 > $OUT/plain_$R.log 2>&1 || { echo "plain bench failed"; exit 1; }
-CASES=${CASES:-"qwz1:quantize_reg_kernel gather4:dequant16_tma_kernel k0:quantize_reg_kernel k1:quantize_reg_kernel k2:drq_tbl_kernel k3:dr_fast_kernel c1q:quantize_reg_kernel c1d:dequant_wide_kernel"}
+CASES=${CASES:-"qwz1:quantize_reg_kernel gather4:dequant16_tma_kernel k0:quantize_reg_kernel k1:quantize_reg_kernel k2:drq_tbl_kernel k3:dr_fast_kernel c1q:quantize_reg_kernel c1d:dequant8_f32_kernel"}
 for CK in $CASES; do
   C=${CK%%:*}
   python tools/profile_kernels.py $C 20 >> $OUT/kernels_$R.jsonl 2>> $OUT/kernels_$R.err || { echo "case $C failed"; exit 1; }
@@ -34,7 +34,7 @@ names = {"qwz1": "quantize_reg_kernel<deq> (fused qwZ self-gather)",
          "gather4": "dequant16_tma_kernel (gather over NVLink)",
          "k0": "quantize_reg_kernel", "k1": "quantize_reg_kernel<swizzle> (qgZ K1)",
          "k2": "drq_tbl_kernel", "k3": "dr_fast_kernel", "c1q": "quantize_reg_kernel<fp32> (config 1)",
-         "c1d": "dequant_wide_kernel (config 1)"}
+         "c1d": "dequant8_f32_kernel (config 1)"}
 scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 for f in glob.glob("/tmp/raw_*.csv"):
     c = os.path.basename(f)[4:-4]
