@@ -15,6 +15,8 @@ cases:
   k3       K3 dequant->f64 fold of 2 INT4/512 (f64 absmax) segments -> fp32
   c1q      config 1: quantize 16M fp32 -> INT8/2048
   c1d      config 1: dequantize 16M INT8/2048 -> fp32
+  qgz1     qgZ of one 256 MiB bf16 bucket in a 1-GPU world (K1 + K2 with the
+           final fp32 output), INT4/512
 """
 
 import json
@@ -96,6 +98,13 @@ def main():
             out = torch.empty(n, dtype=torch.float32, device=dev)
             fn = lambda: zpp.dequant_reduce(q64, torch.float32, out=out, flag=flag)  # noqa: E731
             alg = n_src * (n // 2 + n // 512 * 8) + 4 * n
+    elif case == "qgz1":
+        comm = Communicator(group_size=1, qgz_elems=BUCKET, qgz_stages=1,
+                            qgz_cfg=zpp.QuantConfig(bit_width=4, block_size=512))
+        gr = (torch.randn(BUCKET, generator=g, device=dev) * 1e-3).bfloat16()
+        part = torch.empty(BUCKET, dtype=torch.float32, device=dev)
+        fn = lambda: comm.qgz_reduce_scatter(gr, out=part)  # noqa: E731
+        alg = 2 * BUCKET + BUCKET // 2 + BUCKET // 512 * 4 + BUCKET // 2 + BUCKET // 512 * 4 + 4 * BUCKET
     elif case in ("c1q", "c1d"):
         n = 1 << 24
         x = torch.randn(n, generator=g, device=dev) * 0.02
