@@ -2028,7 +2028,8 @@ __device__ __forceinline__ void fold16_tbl4(const uint2& w, uint32_t slot, doubl
 template <int OBITS, int NSRC, typename FO = void, int NT = NSRC>
 __global__ void __launch_bounds__(256)
 drq_tbl_kernel(SrcTable src, int64_t n, int lg1, int64_t n_blocks_out, uint8_t* __restrict__ codes,
-               double* __restrict__ absmax, uint32_t* __restrict__ flag, FO* __restrict__ final_out = nullptr) {
+               double* __restrict__ absmax, uint32_t* __restrict__ flag, FO* __restrict__ final_out = nullptr,
+               int span_ok = 1) {
   if (comm_aborted(flag)) return;
   __shared__ __align__(256) double tbl_all[8][NT * kTblSlotDoubles];
   __shared__ __align__(64) float fo_all[8][16];
@@ -2042,7 +2043,7 @@ drq_tbl_kernel(SrcTable src, int64_t n, int lg1, int64_t n_blocks_out, uint8_t* 
   // final fp32 output and whole blocks: coalesced layout (store_span_f32);
   // the fp32 table path of drq_epilogue is the only consumer, codes outputs
   // keep the per-lane order their packing needs
-  const bool span = std::is_same<FO, float>::value && OBITS == 4 && (n & 511) == 0;
+  const bool span = span_ok && std::is_same<FO, float>::value && OBITS == 4 && (n & 511) == 0;
   auto load = [&](int64_t b, uint2 (&wv)[NSRC], float (&mv)[NSRC]) {
     const int64_t e0 = b * 512 + (int64_t)tl * 16;
     const bool blk = b < n_blocks_out, ok = blk && e0 < n;
@@ -2095,7 +2096,8 @@ drq_tbl_kernel(SrcTable src, int64_t n, int lg1, int64_t n_blocks_out, uint8_t* 
 // source assigns (see fold16).  Same arithmetic as dr_unit.
 template <int BITS, int NSRC, typename A, typename O, bool TBL = false>
 __global__ void __launch_bounds__(256)
-dr_fast_kernel(SrcTable src, int64_t n, int lg, O* __restrict__ out, double post_scale, uint32_t* __restrict__ flag) {
+dr_fast_kernel(SrcTable src, int64_t n, int lg, O* __restrict__ out, double post_scale, uint32_t* __restrict__ flag,
+               int span_ok = 1) {
   if (comm_aborted(flag)) return;
   static_assert(!TBL || BITS == 4, "product tables are for INT4 sources");
   using V = typename Vec16<BITS>::T;
@@ -2111,7 +2113,7 @@ dr_fast_kernel(SrcTable src, int64_t n, int lg, O* __restrict__ out, double post
   // TBL with fp32 output and whole 512-element warp spans: coalesced layout
   // (see store_span_f32); warp-uniform
   constexpr bool CAN_SPAN = TBL && sizeof(O) == 4;
-  const bool span = CAN_SPAN && (n & 511) == 0;
+  const bool span = CAN_SPAN && span_ok && (n & 511) == 0;
   const int lane = threadIdx.x & 31;
   auto load = [&](int64_t u, V (&wv)[NSRC], A (&mv)[NSRC]) {
     const int64_t ua = TBL ? (u & ~int64_t(31)) : u;

@@ -14,6 +14,17 @@
 
 namespace zpp {
 
+// ZPP_NO_SPAN=1 (development A/B only): fp32 outputs of the INT4 folds in the
+// per-lane layout instead of the warp-coalesced span layout
+static bool span_on() {
+  static const bool v = [] {
+    const char* e = getenv("ZPP_NO_SPAN");
+    return !(e && e[0] == '1');
+  }();
+  return v;
+}
+
+
 // ZPP_FORCE_TMA=1 (development only): route the public K2/K3 entry points to
 // the TMA-fed kernels so they can be timed on local buffers.  Those kernels
 // may read up to 16 bytes past each source slice, which stays inside torch's
@@ -45,7 +56,7 @@ static int run_reduce_fast(const SrcTable& t, int64_t n, int lg, void* out, doub
   auto k = (BITS == 4 && lg >= 9 && !tbl_off()) ? dr_fast_kernel<BITS, NS, A, O, BITS == 4>
                                                 : dr_fast_kernel<BITS, NS, A, O, false>;
   const int grid = grid_for(k, 256, ceil_div(n / 16, 256));
-  k<<<grid, 256, 0, st>>>(t, n, lg, reinterpret_cast<O*>(out), post_scale, flag);
+  k<<<grid, 256, 0, st>>>(t, n, lg, reinterpret_cast<O*>(out), post_scale, flag, span_on() ? 1 : 0);
   return check_cuda(cudaGetLastError(), "dr_fast_kernel launch");
 }
 
@@ -110,16 +121,6 @@ static bool drq_fast_ok(int n_src, int64_t n, int64_t in_block, int64_t out_bloc
          (in_block & (in_block - 1)) == 0 && (n_src == 1 || n_src == 2 || n_src == 4 || n_src == 8);
 }
 
-// ZPP_NO_SPAN=1 (development A/B only): fp32 outputs of the INT4 folds in the
-// per-lane layout instead of the warp-coalesced span layout
-static bool span_on() {
-  static const bool v = [] {
-    const char* e = getenv("ZPP_NO_SPAN");
-    return !(e && e[0] == '1');
-  }();
-  return v;
-}
-
 // ZPP_NO_TBL=1 (development A/B only): INT4 folds without product tables
 bool tbl_off() {
   static const bool off = [] {
@@ -150,7 +151,7 @@ static int run_drq_fast(const SrcTable& t, int n_src, int64_t n, int64_t in_bloc
       auto k = tbl_split() == 2 && NS == 4 ? drq_tbl_kernel<OBITS, NS, FO, (NS == 4 ? 2 : NS)>   \
                                              : drq_tbl_kernel<OBITS, NS, FO>;                   \
       const int grid = grid_for(k, 256, ceil_div(nbo, 8));                                      \
-      k<<<grid, 256, 0, st>>>(t, n, lg1, nbo, codes, absmax, flag, final_out);                  \
+      k<<<grid, 256, 0, st>>>(t, n, lg1, nbo, codes, absmax, flag, final_out, span_on() ? 1 : 0); \
       return check_cuda(cudaGetLastError(), "drq_tbl_kernel launch");                           \
     }                                                                                           \
     auto k = drq_fast_kernel<IBITS, OBITS, NS, FO>;                                             \

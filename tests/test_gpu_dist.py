@@ -79,10 +79,20 @@ def test_eight_gpus_2x4():
     _run(8, 4, 1)
 
 
+def _oversub_allowed():
+    # Ranks whose kernels spin on one another's flags, time-sliced on one GPU,
+    # have raised Xid 109 (context-switch timeout) on this pool's B200s
+    # (B200_PROFILING.md).  These runs passed on 4 B200s during development
+    # (profiles/r2/gpu_dist_large_r2.log); they stay opt-in.
+    if os.environ.get("ZPP_ALLOW_OVERSUBSCRIBE") != "1":
+        pytest.skip("oversubscribed ranks are opt-in (ZPP_ALLOW_OVERSUBSCRIBE=1)")
+
+
 def test_eight_ranks_2x4_oversubscribed():
     """The driver's 8-GPU layout (2 groups x 4, K3 + cross barrier with X = 4)
     on a smaller box: two ranks per GPU, still one process per rank and peer
     memory through CUDA IPC (see ZPP_OVERSUBSCRIBE in dist_worker.py)."""
+    _oversub_allowed()
     n = torch.cuda.device_count()
     if n < 2 or n >= 8:
         pytest.skip("needs 2..7 GPUs (8 run test_eight_gpus_2x4)")
@@ -114,6 +124,7 @@ def test_large_eight_gpus_2x4():
 def test_large_eight_ranks_2x4_oversubscribed():
     """The 2x4 layout at the BASELINE shapes, two ranks per GPU (see
     test_eight_ranks_2x4_oversubscribed)."""
+    _oversub_allowed()
     n = torch.cuda.device_count()
     if n < 4 or n >= 8:
         pytest.skip("needs 4..7 GPUs (8 run test_large_eight_gpus_2x4)")
