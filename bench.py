@@ -395,44 +395,58 @@ def run_ours(args):
                                         "busbw_GBps": 2 * M_PARAMS * (world - 1) / world / t_nccl / 1e9}
     del out
     torch.cuda.empty_cache()
+    def leg(name, fn):
+        """Run one secondary leg; a failure is recorded in the line instead of
+        losing the headline (the legs' arguments are identical on every rank,
+        so a validation error is raised on all of them alike)."""
+        try:
+            extra[name] = fn()
+        except Exception as e:  # noqa: BLE001
+            import traceback
+            traceback.print_exc()
+            extra[name] = {"error": f"{type(e).__name__}: {e}"[:400]}
+            torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+
+    kw = dict(world=world, rank=rank, dev=dev, timed=timed, steps=args.steps, hbm_peak=hbm_peak, synth=synth,
+              sampled=sampled, add_parity=add_parity)
     if "qgz" in sections:
-        extra["qgz"] = qgz_leg(comm=comm, world=world, rank=rank, X=X, dev=dev, timed=timed, steps=args.steps,
-                               hbm_peak=hbm_peak, oversub=oversub, add_parity=add_parity, synth=synth,
-                               sampled=sampled, nccl_reduce_scatter=nccl_reduce_scatter, traffic=traffic)
+        leg("qgz", lambda: qgz_leg(comm=comm, X=X, oversub=oversub, nccl_reduce_scatter=nccl_reduce_scatter,
+                                   traffic=traffic, **kw))
         if world >= 2 and X != world:
             # the same bucket with the whole box as one group (hop 2 a self-send)
-            c1g = Communicator(group_size=world, qgz_elems=QGZ_BUCKET, qgz_stages=1, qgz_cfg=qgz_cfg)
-            extra["qgz_one_group"] = qgz_leg(comm=c1g, world=world, rank=rank, X=world, dev=dev, timed=timed,
-                                             steps=args.steps, hbm_peak=hbm_peak, oversub=oversub,
-                                             add_parity=add_parity, synth=synth, sampled=sampled,
-                                             nccl_reduce_scatter=None, traffic=traffic, parity_name="qgz_one_group")
-            c1g.close()
+            def one_group():
+                c1g = Communicator(group_size=world, qgz_elems=QGZ_BUCKET, qgz_stages=1, qgz_cfg=qgz_cfg)
+                try:
+                    return qgz_leg(comm=c1g, X=world, oversub=oversub, nccl_reduce_scatter=None, traffic=traffic,
+                                   parity_name="qgz_one_group", **kw)
+                finally:
+                    c1g.close()
+            leg("qgz_one_group", one_group)
     comm.close()
     torch.cuda.empty_cache()
     if "config1" in sections:
-        extra["config1_roundtrip_16M_fp32"] = config1_leg(lib=lib, dev=dev, rank=rank, timed_flush=None, steps=args.steps,
-                                                          hbm_peak=hbm_peak, add_parity=add_parity,
-                                                          max_over_ranks=max_over_ranks, barrier=barrier, _lib=_lib)
+        leg("config1_roundtrip_16M_fp32",
+            lambda: config1_leg(lib=lib, dev=dev, rank=rank, timed_flush=None, steps=args.steps, hbm_peak=hbm_peak,
+                                add_parity=add_parity, max_over_ranks=max_over_ranks, barrier=barrier, _lib=_lib))
     if "hpz" in sections:
-        extra["hpz"] = hpz_leg(comm_cls=Communicator, world=world, dev=dev, timed=lambda f: timed(f, args.steps, 2),
-                               oversub=oversub, nccl_allgather=nccl_allgather, synth=synth, sampled=sampled,
-                               add_parity=add_parity, rank=rank)
+        leg("hpz", lambda: hpz_leg(comm_cls=Communicator, world=world, dev=dev,
+                                   timed=lambda f: timed(f, args.steps, 2), oversub=oversub,
+                                   nccl_allgather=nccl_allgather, synth=synth, sampled=sampled,
+                                   add_parity=add_parity, rank=rank))
     if "stream" in sections:
-        extra["qgz_stream_7b"] = stream_leg(comm_cls=Communicator, world=world, rank=rank, X=X, dev=dev, timed=timed,
-                                            steps=args.steps, hbm_peak=hbm_peak, synth=synth, sampled=sampled,
-                                            add_parity=add_parity, zpp=zpp)
+        leg("qgz_stream_7b", lambda: stream_leg(comm_cls=Communicator, X=X, zpp=zpp, **kw))
         if world >= 2 and X != world:
             # the whole box as one group: buckets pipelined (K1 of bucket b+1
             # beside the pull K2 of bucket b)
-            extra["qgz_stream_7b_one_group"] = stream_leg(
-                comm_cls=Communicator, world=world, rank=rank, X=world, dev=dev, timed=timed, steps=args.steps,
-                hbm_peak=hbm_peak, synth=synth, sampled=sampled, add_parity=add_parity, zpp=zpp,
-                parity_name="qgz_stream_one_group")
+            leg("qgz_stream_7b_one_group", lambda: stream_leg(comm_cls=Communicator, X=world, zpp=zpp,
+                                                              parity_name="qgz_stream_one_group", **kw))
     if "step" in sections:
-        extra["zeropp_step_13b"] = step_leg(world=world, rank=rank, dev=dev, timed=timed, steps=args.steps,
-                                            oversub=oversub, comm_cls=Communicator, zpp=zpp, synth=synth,
-                                            sampled=sampled, add_parity=add_parity, nccl_allgather=nccl_allgather,
-                                            nccl_reduce_scatter=nccl_reduce_scatter)
+        leg("zeropp_step_13b", lambda: step_leg(world=world, rank=rank, dev=dev, timed=timed, steps=args.steps,
+                                                oversub=oversub, comm_cls=Communicator, zpp=zpp, synth=synth,
+                                                sampled=sampled, add_parity=add_parity,
+                                                nccl_allgather=nccl_allgather,
+                                                nccl_reduce_scatter=nccl_reduce_scatter))
     kq_gbs = kern["quantize_reg_kernel"]["GBps"]
     extra["quant_kernel_hbm"] = {"kernel": "quantize_reg_kernel (K0: fp16 shard -> INT8/2048 codes + absmax)",
                                  "achieved_GBps": kq_gbs, "frac_of_8TBs_nominal": kq_gbs / 8000.0,
