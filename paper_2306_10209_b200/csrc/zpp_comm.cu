@@ -700,6 +700,12 @@ int zpp_qgz_reduce_scatter_buckets(zpp_comm_t c, size_t sym_offset, const void* 
   }();
   const int64_t epl = dtype == ZPP_F32 ? 32 : 64;
   const bool want_push = mode_env == 1 || (mode_env == 0 && Y > 1);
+  // hop 2 by push (K2 stores into the receivers' slots): ZPP_QGZ_HOP2=pull|push
+  static const int hop2_env = [] {
+    const char* e = getenv("ZPP_QGZ_HOP2");
+    return !e ? 0 : (e[1] == 'u' && e[2] == 's') ? 1 : 2;  // 1 push, 2 pull
+  }();
+  const bool hop2_push = hop2_env != 2;
   const bool push = want_push && dtype != ZPP_F64 && X <= 8 && intra_block % epl == 0 &&
                     intra_block / epl >= 2 && intra_block / epl <= 32 &&
                     ((intra_block / epl) & (intra_block / epl - 1)) == 0;
@@ -803,7 +809,27 @@ int zpp_qgz_reduce_scatter_buckets(zpp_comm_t c, size_t sym_offset, const void* 
       }
     }
     bool handled = false;
-    if (in_abs == ZPP_F32 && !push)
+    // Hop 2 by push (with a pushed hop 1): K2 stores segment c of its output
+    // straight into rank (c, loc)'s hop-2 receive slot for this node, over
+    // NVLink, and K3 folds local HBM.  The slot was last read by that rank's
+    // K3 of the unit before the previous one, which precedes its cross
+    // barrier of the previous unit, which this K2 follows.
+    bool hop2_pushed = false;
+    if (push && hop2_push) {
+      HopDst hd{};
+      const size_t seg_code_bytes = (size_t)code_bytes(L, inter_bits, inter_block);
+      for (int g = 0; g < Y; ++g) {
+        uint8_t* p = c->peers[g * X + loc] + base;
+        hd.codes[g] = p + l.hop_codes + seg_code_bytes * node;
+        hd.absmax[g] = reinterpret_cast<double*>(p + l.hop_abs + (size_t)(L / inter_block) * 8 * node);
+      }
+      hd.seg_blocks = L / 512;
+      rc = launch_drq_hop(codes, absmax, X, msg_elems, intra_bits, intra_block, inter_bits, inter_block, hd, flag, st,
+                          &hop2_pushed);
+      if (rc) return rc;
+      handled = hop2_pushed;
+    }
+    if (!handled && in_abs == ZPP_F32 && !push)
       rc = launch_drq_tma(codes, absmax, X, msg_elems, intra_bits, intra_block, inter_bits, inter_block,
                           c->local + base + l.hop_codes, reinterpret_cast<double*>(c->local + base + l.hop_abs),
                           nullptr, 0, flag, st, &handled);
@@ -818,15 +844,17 @@ int zpp_qgz_reduce_scatter_buckets(zpp_comm_t c, size_t sym_offset, const void* 
     rc = barrier(c, 2, kBarrierTimeoutMs, flag, st);
     if (rc) return rc;
     trace_mark(c, TR_BARRIER, st);
-    // K3: pull segment `node` from the rank with my local index in every group
+    // K3: segment `node` from the rank with my local index in every group --
+    // already in my hop-2 slots [g] when hop 2 was pushed, else pulled
     for (int g = 0; g < Y; ++g) {
-      const uint8_t* p = c->peers[g * X + loc] + base;
-      codes[g] = p + l.hop_codes + (size_t)code_bytes(L, inter_bits, inter_block) * node;
-      absmax[g] = p + l.hop_abs + (size_t)(L / inter_block) * 8 * node;
+      const uint8_t* p = hop2_pushed ? c->local + base : c->peers[g * X + loc] + base;
+      const int slot = hop2_pushed ? g : node;
+      codes[g] = p + l.hop_codes + (size_t)code_bytes(L, inter_bits, inter_block) * slot;
+      absmax[g] = p + l.hop_abs + (size_t)(L / inter_block) * 8 * slot;
     }
     handled = false;
-    rc = launch_dr_tma(codes, absmax, Y, L, inter_bits, inter_block,
-                       out_s, out_dtype, flag, st, &handled);
+    if (!hop2_pushed)
+      rc = launch_dr_tma(codes, absmax, Y, L, inter_bits, inter_block, out_s, out_dtype, flag, st, &handled);
     if (rc) return rc;
     if (!handled)
       rc = launch_dequant_reduce(codes, absmax, ZPP_F64, Y, L, inter_bits, inter_block,

@@ -46,6 +46,10 @@ int launch_drq(const void* const* codes, const void* const* absmax, int absmax_d
                int in_bits, int64_t in_block, int out_bits, int64_t out_block, uint8_t* out_codes,
                double* out_absmax, void* workspace, size_t ws_bytes, uint32_t* flag, cudaStream_t st,
                bool validate = true);
+struct HopDst;  // zpp_kernels.cuh
+int launch_drq_hop(const void* const* codes, const void* const* absmax, int n_src, int64_t n, int in_bits,
+                   int64_t in_block, int out_bits, int64_t out_block, const HopDst& hop, uint32_t* flag,
+                   cudaStream_t st, bool* handled);
 int launch_drq_final(const void* const* codes, const void* const* absmax, int absmax_dtype, int n_src, int64_t n,
                      int in_bits, int64_t in_block, int out_bits, int64_t out_block, double* out_absmax, void* out,
                      int out_dtype, uint32_t* flag, cudaStream_t st, bool* handled);

@@ -2025,11 +2025,22 @@ __device__ __forceinline__ void fold16_tbl4(const uint2& w, uint32_t slot, doubl
 // multiples of 512 (one scale per warp and source).  Every lane loads the
 // block absmax even past the end of a partial last block, so the table inputs
 // are warp-uniform.
-template <int OBITS, int NSRC, typename FO = void, int NT = NSRC>
+// Hop-2 destinations of K2's output when hop 2 is pushed: segment c (L
+// elements = seg_blocks output blocks of 512) of this rank's K2 output goes to
+// rank (c, loc)'s hop-2 receive slot for this rank's node, so that rank's K3
+// folds local HBM.  Pointers may be peers' symmetric memory (NVLink stores).
+constexpr int kMaxHop = 8;
+struct HopDst {
+  uint8_t* codes[kMaxHop];   // slot start of segment c's codes (256 B per output block)
+  double* absmax[kMaxHop];   // ... and of its f64 absmax
+  int64_t seg_blocks;        // output blocks per segment (L / 512)
+};
+
+template <int OBITS, int NSRC, typename FO = void, int NT = NSRC, bool HOP = false>
 __global__ void __launch_bounds__(256)
 drq_tbl_kernel(SrcTable src, int64_t n, int lg1, int64_t n_blocks_out, uint8_t* __restrict__ codes,
                double* __restrict__ absmax, uint32_t* __restrict__ flag, FO* __restrict__ final_out = nullptr,
-               int span_ok = 1) {
+               int span_ok = 1, HopDst hop = HopDst{}) {
   if (comm_aborted(flag)) return;
   __shared__ __align__(256) double tbl_all[8][NT * kTblSlotDoubles];
   __shared__ __align__(64) float fo_all[8][16];
@@ -2083,10 +2094,21 @@ drq_tbl_kernel(SrcTable src, int64_t n, int lg1, int64_t n_blocks_out, uint8_t* 
       if (j < NT) fold16_tbl4<false>(w[j], slot0 + j * 256, acc, bad);
       else fold16<4, true>(w[j], div_q_f32<7>(m[j]), acc, bad);
     }
-    drq_epilogue<OBITS, FO>(acc, b, tl, e0, active, u, codes, absmax, flag, final_out, fo_all[threadIdx.x >> 5],
-                            span);
+    if constexpr (HOP) {
+      // block b of segment c lands at block b - c*seg_blocks of c's slot;
+      // the epilogue indexes codes by unit (b*32 + tl) and absmax by b
+      const int64_t c = b / hop.seg_blocks;
+      const int64_t shift = c * hop.seg_blocks;
+      uint8_t* cb = hop.codes[c] - shift * (512 * OBITS / 8);
+      double* ab = hop.absmax[c] - shift;
+      drq_epilogue<OBITS, FO>(acc, b, tl, e0, active, u, cb, ab, flag, final_out, fo_all[threadIdx.x >> 5], span);
+    } else {
+      drq_epilogue<OBITS, FO>(acc, b, tl, e0, active, u, codes, absmax, flag, final_out, fo_all[threadIdx.x >> 5],
+                              span);
+    }
   }
   if (bad) raise_flag(flag, FLAG_BADCODE);
+  if constexpr (HOP) __threadfence_system();  // the stores to peers are performed before the cross barrier's release
 }
 
 // K3 fixed fan-in fast path (the qgZ hop-2 fold, zs/collectives.py:536-544):

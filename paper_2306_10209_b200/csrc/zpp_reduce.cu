@@ -151,7 +151,7 @@ static int run_drq_fast(const SrcTable& t, int n_src, int64_t n, int64_t in_bloc
       auto k = tbl_split() == 2 && NS == 4 ? drq_tbl_kernel<OBITS, NS, FO, (NS == 4 ? 2 : NS)>   \
                                              : drq_tbl_kernel<OBITS, NS, FO>;                   \
       const int grid = grid_for(k, 256, ceil_div(nbo, 8));                                      \
-      k<<<grid, 256, 0, st>>>(t, n, lg1, nbo, codes, absmax, flag, final_out, span_on() ? 1 : 0); \
+      k<<<grid, 256, 0, st>>>(t, n, lg1, nbo, codes, absmax, flag, final_out, span_on() ? 1 : 0, HopDst{}); \
       return check_cuda(cudaGetLastError(), "drq_tbl_kernel launch");                           \
     }                                                                                           \
     auto k = drq_fast_kernel<IBITS, OBITS, NS, FO>;                                             \
@@ -202,6 +202,39 @@ static int drq_block(const SrcTable& t, int n_src, int64_t n, int64_t in_block, 
   }
 #undef ZPP_RUN
   return fail(ZPP_ERR_VALIDATION, "no register path for this output block");
+}
+
+// K2 with its output pushed to the hop-2 receivers (HopDst): INT4 -> INT4/512
+// through the product tables only; *handled = false otherwise.
+int launch_drq_hop(const void* const* codes, const void* const* absmax, int n_src, int64_t n, int in_bits,
+                   int64_t in_block, int out_bits, int64_t out_block, const HopDst& hop, uint32_t* flag,
+                   cudaStream_t st, bool* handled) {
+  *handled = false;
+  if (n == 0 || in_bits != 4 || out_bits != 4 || out_block != 512 || in_block % 512 != 0 || tbl_off()) return ZPP_OK;
+  if (n % 512 != 0 || hop.seg_blocks <= 0) return ZPP_OK;
+  for (int i = 0; i < n_src; ++i)
+    if (reinterpret_cast<uintptr_t>(codes[i]) % 8) return ZPP_OK;
+  SrcTable t;
+  int rc = fill_table(t, codes, absmax, n_src);
+  if (rc) return rc;
+  const int lg1 = __builtin_ctzll((unsigned long long)in_block);
+  const int64_t nbo = n / 512;
+#define ZPP_HOP(NS)                                                                              \
+  {                                                                                              \
+    auto k = drq_tbl_kernel<4, NS, void, NS, true>;                                              \
+    const int grid = grid_for(k, 256, ceil_div(nbo, 8));                                         \
+    k<<<grid, 256, 0, st>>>(t, n, lg1, nbo, nullptr, nullptr, flag, nullptr, 1, hop);           \
+    *handled = true;                                                                             \
+    return check_cuda(cudaGetLastError(), "drq_tbl_kernel<hop> launch");                         \
+  }
+  switch (n_src) {
+    case 1: ZPP_HOP(1)
+    case 2: ZPP_HOP(2)
+    case 4: ZPP_HOP(4)
+    case 8: ZPP_HOP(8)
+  }
+#undef ZPP_HOP
+  return ZPP_OK;
 }
 
 int launch_drq(const void* const* codes, const void* const* absmax, int absmax_dtype, int n_src, int64_t n,
