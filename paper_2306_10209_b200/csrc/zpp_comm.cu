@@ -700,12 +700,15 @@ int zpp_qgz_reduce_scatter_buckets(zpp_comm_t c, size_t sym_offset, const void* 
   }();
   const int64_t epl = dtype == ZPP_F32 ? 32 : 64;
   const bool want_push = mode_env == 1 || (mode_env == 0 && Y > 1);
-  // hop 2 by push (K2 stores into the receivers' slots): ZPP_QGZ_HOP2=pull|push
+  // Hop 2 by push (K2 stores into the receivers' slots, K3 local) is opt-in
+  // (ZPP_QGZ_HOP2=push): measured no faster at 2x2 (193.2 vs 193.5 us per
+  // 256 MiB bucket) and slower at 2x1 (270 vs 255 us) than K3 pulling the
+  // segment with TMA (profiles/r2/qgz_hop2_push_r2.jsonl).
   static const int hop2_env = [] {
     const char* e = getenv("ZPP_QGZ_HOP2");
     return !e ? 0 : (e[1] == 'u' && e[2] == 's') ? 1 : 2;  // 1 push, 2 pull
   }();
-  const bool hop2_push = hop2_env != 2;
+  const bool hop2_push = hop2_env == 1;
   const bool push = want_push && dtype != ZPP_F64 && X <= 8 && intra_block % epl == 0 &&
                     intra_block / epl >= 2 && intra_block / epl <= 32 &&
                     ((intra_block / epl) & (intra_block / epl - 1)) == 0;

@@ -2054,7 +2054,9 @@ drq_tbl_kernel(SrcTable src, int64_t n, int lg1, int64_t n_blocks_out, uint8_t* 
   // final fp32 output and whole blocks: coalesced layout (store_span_f32);
   // the fp32 table path of drq_epilogue is the only consumer, codes outputs
   // keep the per-lane order their packing needs
-  const bool span = span_ok && std::is_same<FO, float>::value && OBITS == 4 && (n & 511) == 0;
+  // (not with one source: the four 16-bit loads cost more than the coalesced
+  // stores gain there, 231 vs 224 us for the 1-GPU qgZ bucket)
+  const bool span = span_ok && NSRC > 1 && std::is_same<FO, float>::value && OBITS == 4 && (n & 511) == 0;
   auto load = [&](int64_t b, uint2 (&wv)[NSRC], float (&mv)[NSRC]) {
     const int64_t e0 = b * 512 + (int64_t)tl * 16;
     const bool blk = b < n_blocks_out, ok = blk && e0 < n;

@@ -61,16 +61,16 @@ def test_four_gpus_1x4():
     _run(4, 4, 1)
 
 
-@pytest.mark.parametrize("mode", ["push", "pull", "push-hop2pull"])
+@pytest.mark.parametrize("mode", ["push", "pull", "push-hop2push"])
 def test_qgz_hop1_modes(mode):
     """Both hop-1 transports (K1 pushing with TMA bulk stores / K2 pulling)
     on the layouts whose default is the other one: 1xN defaults to pull, 2x2
     to push (see zpp_qgz_reduce_scatter); and with a pushed hop 1, hop 2
-    pulled by K3 instead of pushed by K2 (ZPP_QGZ_HOP2=pull)."""
+    pushed by K2 into the receivers' slots (ZPP_QGZ_HOP2=push, opt-in)."""
     n = torch.cuda.device_count()
     env = {"ZPP_QGZ_MODE": mode.split("-")[0]}
-    if mode.endswith("hop2pull"):
-        env["ZPP_QGZ_HOP2"] = "pull"
+    if mode.endswith("hop2push"):
+        env["ZPP_QGZ_HOP2"] = "push"
     _run(2, 2, 2, env=env)
     _run(2, 1, 2, env=env)
     if n >= 4:
