@@ -2097,13 +2097,12 @@ drq_tbl_kernel(SrcTable src, int64_t n, int lg1, int64_t n_blocks_out, uint8_t* 
       else fold16<4, true>(w[j], div_q_f32<7>(m[j]), acc, bad);
     }
     if constexpr (HOP) {
-      // block b of segment c lands at block b - c*seg_blocks of c's slot;
-      // the epilogue indexes codes by unit (b*32 + tl) and absmax by b
+      // block b of segment c lands at block b - c*seg_blocks of c's slot (the
+      // epilogue indexes codes by unit, 32 per block, and absmax by block)
       const int64_t c = b / hop.seg_blocks;
       const int64_t shift = c * hop.seg_blocks;
-      uint8_t* cb = hop.codes[c] - shift * (512 * OBITS / 8);
-      double* ab = hop.absmax[c] - shift;
-      drq_epilogue<OBITS, FO>(acc, b, tl, e0, active, u, cb, ab, flag, final_out, fo_all[threadIdx.x >> 5], span);
+      drq_epilogue<OBITS, FO>(acc, b - shift, tl, e0, active, u - shift * 32, hop.codes[c], hop.absmax[c], flag,
+                              final_out, fo_all[threadIdx.x >> 5], span);
     } else {
       drq_epilogue<OBITS, FO>(acc, b, tl, e0, active, u, codes, absmax, flag, final_out, fo_all[threadIdx.x >> 5],
                               span);
