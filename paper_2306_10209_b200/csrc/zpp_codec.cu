@@ -56,7 +56,7 @@ static int run_qreg(const T* x, const Addr& addr, int64_t n_blocks, uint8_t* cod
                     cudaStream_t st) {
   auto k = quantize_reg_kernel<T, BITS, LANES, EPL, Addr>;
   const int grid = grid_for(k, 256, ceil_div(n_blocks, 256 / LANES));
-  k<<<grid, 256, 0, st>>>(x, addr, n_blocks, codes, absmax, flag, nullptr);
+  launch_k(k, grid, 256, 0, st, x, addr, n_blocks, codes, absmax, flag, nullptr);
   return check_cuda(cudaGetLastError(), "quantize_reg_kernel launch");
 }
 
@@ -140,7 +140,7 @@ static bool qdeq_t(const T* x, int64_t n, int64_t block, uint8_t* codes, float* 
   {                                                                                       \
     auto k = quantize_reg_kernel<T, BITS, L, (int)EPL, PlainAddr, true>;                  \
     const int grid = grid_for(k, 256, ceil_div(nb, 256 / L));                             \
-    k<<<grid, 256, 0, st>>>(x, addr, nb, codes, absmax, flag, out);                       \
+    launch_k(k, grid, 256, 0, st, x, addr, nb, codes, absmax, flag, out);                  \
     *rc = check_cuda(cudaGetLastError(), "quantize_reg_kernel<deq> launch");              \
     return true;                                                                          \
   }
@@ -192,7 +192,7 @@ static int run_qpush(const T* x, const SwizzleAddr& addr, int n_msg, int first, 
   auto k = quantize_push_kernel<T, BITS, LANES, EPL>;
   const int64_t tiles = ceil_div((int64_t)dst.mb.d, PushTile<LANES, EPL, BITS>::WT) * n_msg;
   const int grid = grid_for(k, 256, ceil_div(tiles, 8));
-  k<<<grid, 256, 0, st>>>(x, addr, n_msg, first, dst, flag);
+  launch_k(k, grid, 256, 0, st, x, addr, n_msg, first, dst, flag);
   return check_cuda(cudaGetLastError(), "quantize_push_kernel launch");
 }
 
@@ -267,7 +267,7 @@ static int run_gather(const SrcTable& t, int n_src, int rot, int64_t shard_len, 
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 256, smem);
       const int64_t units = ceil_div(shard_len, 128 / BITS);
       const int grid = (int)std::min<int64_t>((int64_t)sm_budget() * occ_capped(occ), ceil_div(units, TU) * n_src);
-      k<<<grid, 256, smem, st>>>(t, n_src, rot, shard_len, block, reinterpret_cast<O*>(out),
+      launch_k(k, grid, 256, smem, st, t, n_src, rot, shard_len, block, reinterpret_cast<O*>(out),
                                  reinterpret_cast<O*>(sec_out), sec_lo, sec_len, vec_ok, flag, out_stride);
       return check_cuda(cudaGetLastError(), "dequant16_tma_kernel launch");
     }
@@ -275,7 +275,7 @@ static int run_gather(const SrcTable& t, int n_src, int rot, int64_t shard_len, 
       auto k = dequant16_kernel<BITS, O>;
       const int64_t tiles = ceil_div(ceil_div(shard_len, 128 / BITS), 32 * (BITS == 8 ? 2 : 1)) * n_src;
       const int grid = grid_for(k, 256, ceil_div(tiles, 8));
-      k<<<grid, 256, 0, st>>>(t, n_src, rot, shard_len, block, reinterpret_cast<O*>(out),
+      launch_k(k, grid, 256, 0, st, t, n_src, rot, shard_len, block, reinterpret_cast<O*>(out),
                               reinterpret_cast<O*>(sec_out), sec_lo, sec_len, vec_ok, flag, out_stride);
       return check_cuda(cudaGetLastError(), "dequant16_kernel launch");
     }
@@ -287,7 +287,7 @@ static int run_gather(const SrcTable& t, int n_src, int rot, int64_t shard_len, 
     if (ok) {
       auto k = dequant8_f32_kernel<8>;
       const int grid = grid_for(k, 256, ceil_div(shard_len / 4, 256 * 4));
-      k<<<grid, 256, 0, st>>>(t, n_src, shard_len, block, reinterpret_cast<float*>(out),
+      launch_k(k, grid, 256, 0, st, t, n_src, shard_len, block, reinterpret_cast<float*>(out),
                               out_stride ? out_stride : shard_len, flag);
       return check_cuda(cudaGetLastError(), "dequant8_f32_kernel launch");
     }
@@ -301,7 +301,7 @@ static int run_gather(const SrcTable& t, int n_src, int rot, int64_t shard_len, 
     if (wide) {
       auto k = dequant_wide_kernel<BITS, O>;
       const int grid = grid_for(k, 256, ceil_div(shard_len / E, 256));
-      k<<<grid, 256, 0, st>>>(t, n_src, shard_len, block, reinterpret_cast<O*>(out),
+      launch_k(k, grid, 256, 0, st, t, n_src, shard_len, block, reinterpret_cast<O*>(out),
                               out_stride ? out_stride : shard_len, flag);
       return check_cuda(cudaGetLastError(), "dequant_wide_kernel launch");
     }
@@ -309,7 +309,7 @@ static int run_gather(const SrcTable& t, int n_src, int rot, int64_t shard_len, 
   auto k = dequant_gather_kernel<BITS, A, O>;
   const int64_t tiles = ceil_div(ceil_div(shard_len, 8), 32 * 4) * n_src;
   const int grid = grid_for(k, 256, ceil_div(tiles, 8));
-  k<<<grid, 256, 0, st>>>(t, n_src, rot, shard_len, block, reinterpret_cast<O*>(out), reinterpret_cast<O*>(sec_out),
+  launch_k(k, grid, 256, 0, st, t, n_src, rot, shard_len, block, reinterpret_cast<O*>(out), reinterpret_cast<O*>(sec_out),
                           sec_lo, sec_len, vec_ok, flag, out_stride);
   return check_cuda(cudaGetLastError(), "dequant_gather_kernel launch");
 }

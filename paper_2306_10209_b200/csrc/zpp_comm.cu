@@ -214,7 +214,7 @@ static int barrier(zpp_comm_t c, int scope, int timeout_ms, uint32_t* flag, cuda
     a.local[i] = c->flag_slot(c->rank, scope, m[i]);
   }
   const uint64_t to = (uint64_t)(timeout_ms > 0 ? timeout_ms : 60000) * 1000000ull;
-  barrier_kernel<<<1, 64, 0, st>>>(a, (int)m.size(), e, to, flag);
+  launch_k(barrier_kernel, 1, 64, 0, st, a, (int)m.size(), e, to, flag);
   return check_cuda(cudaGetLastError(), "barrier_kernel launch");
 }
 
@@ -392,6 +392,7 @@ int zpp_qwz_allgather_next(zpp_comm_t c, size_t sym_offset, const void* shard, i
   const size_t region = qwz_region(shard_len, bits, block, ZPP_F64);
   if (sym_offset + 2 * region > c->sym_bytes) return fail(ZPP_ERR_VALIDATION, "symmetric buffer too small for qwZ");
   if (shard_len == 0) return ZPP_OK;
+  PdlScope pdl(true);  // K0 -> barrier -> gather overlap their launches
   trace_reset(c);
   trace_mark(c, TR_BEGIN, reinterpret_cast<cudaStream_t>(stream));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
@@ -515,6 +516,7 @@ int zpp_hpz_allgather(zpp_comm_t c, size_t sym_offset, int64_t sec_len, int elem
   if (sym_offset + (size_t)seg > c->sym_bytes) return fail(ZPP_ERR_VALIDATION, "symmetric buffer too small for hpZ");
   if (seg == 0) return ZPP_OK;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  PdlScope pdl(true);  // barrier -> gather overlap their launches
   rc = barrier(c, 1, kBarrierTimeoutMs, reinterpret_cast<uint32_t*>(errflag), st);
   if (rc) return rc;
   std::vector<int> m = c->members(1);
@@ -530,12 +532,12 @@ int zpp_hpz_allgather(zpp_comm_t c, size_t sym_offset, int64_t sec_len, int elem
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gather_copy_tma_kernel, 256, smem);
     const int64_t tiles = ceil_div(seg, kCopyTile) * n;
     const int grid = (int)std::min<int64_t>((int64_t)sm_count() * std::max(occ, 1), tiles);
-    gather_copy_tma_kernel<<<grid, 256, smem, st>>>(t, n, c->rank % c->group, seg, reinterpret_cast<uint8_t*>(out),
+    launch_k(gather_copy_tma_kernel, grid, 256, smem, st, t, n, c->rank % c->group, seg, reinterpret_cast<uint8_t*>(out),
                                                     reinterpret_cast<const uint32_t*>(errflag));
     return check_cuda(cudaGetLastError(), "gather_copy_tma_kernel launch");
   }
   const int grid = (int)std::min<int64_t>(4 * sm_count(), std::max<int64_t>(1, ceil_div(seg * n, 16 * 256)));
-  gather_copy_kernel<<<grid, 256, 0, st>>>(t, n, c->rank % c->group, seg, reinterpret_cast<uint8_t*>(out), vec,
+  launch_k(gather_copy_kernel, grid, 256, 0, st, t, n, c->rank % c->group, seg, reinterpret_cast<uint8_t*>(out), vec,
                                            reinterpret_cast<const uint32_t*>(errflag));
   return check_cuda(cudaGetLastError(), "gather_copy_kernel launch");
 }
@@ -642,6 +644,7 @@ int zpp_qgz_reduce_scatter_buckets(zpp_comm_t c, size_t sym_offset, const void* 
     if ((rc = barrier(c, 0, kBarrierTimeoutMs, flag, st))) return rc;
   }
   c->qgz_region = l.region;
+  PdlScope pdl(true);  // K1 -> barrier -> K2 -> barrier -> K3 overlap their launches
   trace_reset(c);
   trace_mark(c, TR_BEGIN, st);
   const uint64_t use0 = c->qgz_uses;

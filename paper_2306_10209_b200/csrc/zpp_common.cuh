@@ -32,7 +32,16 @@ __device__ __forceinline__ void raise_flag(uint32_t* flag, uint32_t bit) {
 // data kernel sharing the flag returns without touching its buffers until the
 // host clears the condition (Communicator.recover()).  One load per thread at
 // kernel entry.
+//
+// It is also every kernel's programmatic-dependent-launch point: a kernel the
+// communicator launches with programmatic stream serialization (launch_k under
+// PdlScope) may be scheduled while its predecessor is still finishing, so it
+// first waits for the predecessor grid to complete and its memory to be
+// visible (griddepcontrol.wait), then lets its own successor be scheduled
+// (griddepcontrol.launch_dependents).  Both are no-ops for a normal launch.
 __device__ __forceinline__ bool comm_aborted(const uint32_t* flag) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   return flag && (*reinterpret_cast<const volatile uint32_t*>(flag) & FLAG_TIMEOUT);
 }
 

@@ -1,6 +1,9 @@
 // Launch helpers shared by the host translation units.
 #pragma once
 
+#include <cstdlib>
+#include <utility>
+
 #include "zpp_internal.h"
 #include "zpp_kernels.cuh"
 
@@ -41,6 +44,47 @@ inline bool balanced_grids() {
     return !(e && e[0] == '0');
   }();
   return v;
+}
+
+// Programmatic dependent launch for the communicator's kernel chains
+// (K0 -> barrier -> gather, K1 -> barrier -> K2 -> barrier -> K3): under a
+// PdlScope, launch_k sets cudaLaunchAttributeProgrammaticStreamSerialization,
+// so each kernel's launch and CTA ramp overlap the tail of the one before it;
+// every such kernel waits for its predecessor at entry (comm_aborted).
+// ZPP_PDL=0 turns it off (A/B).
+inline thread_local bool t_pdl = false;
+
+inline bool pdl_enabled() {
+  static const bool v = [] {
+    const char* e = getenv("ZPP_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+
+struct PdlScope {
+  bool saved;
+  explicit PdlScope(bool on) : saved(t_pdl) { t_pdl = on && pdl_enabled(); }
+  ~PdlScope() { t_pdl = saved; }
+};
+
+template <typename... KArgs, typename... Args>
+inline void launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+  if (!t_pdl) {
+    k<<<grid, block, smem, st>>>(std::forward<Args>(args)...);
+    return;
+  }
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
 }
 
 // one resident wave of CTAs (persistent-style grid-stride), capped by work

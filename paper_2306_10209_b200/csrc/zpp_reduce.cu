@@ -56,7 +56,7 @@ static int run_reduce_fast(const SrcTable& t, int64_t n, int lg, void* out, doub
   auto k = (BITS == 4 && lg >= 9 && !tbl_off()) ? dr_fast_kernel<BITS, NS, A, O, BITS == 4>
                                                 : dr_fast_kernel<BITS, NS, A, O, false>;
   const int grid = grid_for(k, 256, ceil_div(n / 16, 256));
-  k<<<grid, 256, 0, st>>>(t, n, lg, reinterpret_cast<O*>(out), post_scale, flag, span_on() ? 1 : 0);
+  launch_k(k, grid, 256, 0, st, t, n, lg, reinterpret_cast<O*>(out), post_scale, flag, span_on() ? 1 : 0);
   return check_cuda(cudaGetLastError(), "dr_fast_kernel launch");
 }
 
@@ -78,12 +78,12 @@ static int run_reduce(const SrcTable& t, int n_src, int64_t n, int64_t block, vo
   if (n % 16 == 0 && block % 16 == 0 && aligned16(out) && codes_aligned(t, n_src, BITS)) {
     auto k = validate ? dequant_reduce16_kernel<BITS, A, O, true> : dequant_reduce16_kernel<BITS, A, O, false>;
     const int grid = grid_for(k, 256, ceil_div(n / 16, 256));
-    k<<<grid, 256, 0, st>>>(t, n_src, n, block, reinterpret_cast<O*>(out), post_scale, flag);
+    launch_k(k, grid, 256, 0, st, t, n_src, n, block, reinterpret_cast<O*>(out), post_scale, flag);
     return check_cuda(cudaGetLastError(), "dequant_reduce16_kernel launch");
   }
   auto k = dequant_reduce_kernel<BITS, A, O>;
   const int grid = grid_for(k, 256, ceil_div(n, 8 * 32 * 2 * 8));
-  k<<<grid, 256, 0, st>>>(t, n_src, n, block, reinterpret_cast<O*>(out), post_scale, aligned16(out), flag);
+  launch_k(k, grid, 256, 0, st, t, n_src, n, block, reinterpret_cast<O*>(out), post_scale, aligned16(out), flag);
   return check_cuda(cudaGetLastError(), "dequant_reduce_kernel launch");
 }
 
@@ -151,12 +151,12 @@ static int run_drq_fast(const SrcTable& t, int n_src, int64_t n, int64_t in_bloc
       auto k = tbl_split() == 2 && NS == 4 ? drq_tbl_kernel<OBITS, NS, FO, (NS == 4 ? 2 : NS)>   \
                                              : drq_tbl_kernel<OBITS, NS, FO>;                   \
       const int grid = grid_for(k, 256, ceil_div(nbo, 8));                                      \
-      k<<<grid, 256, 0, st>>>(t, n, lg1, nbo, codes, absmax, flag, final_out, span_on() ? 1 : 0, HopDst{}); \
+      launch_k(k, grid, 256, 0, st, t, n, lg1, nbo, codes, absmax, flag, final_out, span_on() ? 1 : 0, HopDst{}); \
       return check_cuda(cudaGetLastError(), "drq_tbl_kernel launch");                           \
     }                                                                                           \
     auto k = drq_fast_kernel<IBITS, OBITS, NS, FO>;                                             \
     const int grid = grid_for(k, 256, ceil_div(nbo, 8));                                        \
-    k<<<grid, 256, 0, st>>>(t, n, lg1, nbo, codes, absmax, flag, final_out);                    \
+    launch_k(k, grid, 256, 0, st, t, n, lg1, nbo, codes, absmax, flag, final_out);                    \
     return check_cuda(cudaGetLastError(), "drq_fast_kernel launch");                            \
   }
   switch (n_src) {
@@ -178,12 +178,12 @@ static int run_drq(const SrcTable& t, int n_src, int64_t n, int64_t in_block, in
   if (n % 16 == 0 && in_block % 16 == 0 && codes_aligned(t, n_src, IBITS)) {
     auto k = validate ? drq16_kernel<IBITS, IA, OBITS, LANES, true> : drq16_kernel<IBITS, IA, OBITS, LANES, false>;
     const int grid = grid_for(k, 256, ceil_div(nbo, 256 / LANES));
-    k<<<grid, 256, 0, st>>>(t, n_src, n, in_block, nbo, codes, absmax, flag, nullptr);
+    launch_k(k, grid, 256, 0, st, t, n_src, n, in_block, nbo, codes, absmax, flag, nullptr);
     return check_cuda(cudaGetLastError(), "drq16_kernel launch");
   }
   auto k = drq_reg_kernel<IBITS, IA, OBITS, LANES>;
   const int grid = grid_for(k, 256, ceil_div(nbo, 256 / LANES));
-  k<<<grid, 256, 0, st>>>(t, n_src, n, in_block, nbo, codes, absmax, flag);
+  launch_k(k, grid, 256, 0, st, t, n_src, n, in_block, nbo, codes, absmax, flag);
   return check_cuda(cudaGetLastError(), "drq_reg_kernel launch");
 }
 
@@ -223,7 +223,7 @@ int launch_drq_hop(const void* const* codes, const void* const* absmax, int n_sr
   {                                                                                              \
     auto k = drq_tbl_kernel<4, NS, void, NS, true>;                                              \
     const int grid = grid_for(k, 256, ceil_div(nbo, 8));                                         \
-    k<<<grid, 256, 0, st>>>(t, n, lg1, nbo, nullptr, nullptr, flag, nullptr, 1, hop);           \
+    launch_k(k, grid, 256, 0, st, t, n, lg1, nbo, nullptr, nullptr, flag, nullptr, 1, hop);      \
     *handled = true;                                                                             \
     return check_cuda(cudaGetLastError(), "drq_tbl_kernel<hop> launch");                         \
   }
@@ -305,7 +305,7 @@ int launch_drq_final(const void* const* codes, const void* const* absmax, int ab
     }                                                                                                 \
     auto k = drq16_kernel<IB, IA, OB, 32, false, FO>;                                                 \
     const int grid = grid_for(k, 256, ceil_div(nbo, 8));                                              \
-    k<<<grid, 256, 0, st>>>(t, n_src, n, in_block, nbo, nullptr, out_absmax, flag,                    \
+    launch_k(k, grid, 256, 0, st, t, n_src, n, in_block, nbo, nullptr, out_absmax, flag,                    \
                             reinterpret_cast<FO*>(out));                                              \
     *handled = true;                                                                                  \
     return check_cuda(cudaGetLastError(), "drq16_kernel<final> launch");                              \
@@ -369,7 +369,7 @@ static int run_drq_tma(const SrcTable& t, int64_t n, int64_t in_block, uint8_t* 
                : drq_tma_kernel<IB, OB, NS, FO, kTmaStages, false>;
   size_t smem = 0;
   const int grid = tma_grid(k, tt, ceil_div(n / 16, tt.tu), &smem);
-  k<<<grid, 256, smem, st>>>(t, n, tt, codes, absmax, flag, fo);
+  launch_k(k, grid, 256, smem, st, t, n, tt, codes, absmax, flag, fo);
   return check_cuda(cudaGetLastError(), "drq_tma_kernel launch");
 }
 
@@ -426,7 +426,7 @@ static int run_dr_tma(const SrcTable& t, int64_t n, int64_t block, O* out, uint3
                : dr_tma_kernel<B, NS, O, kTmaStages, false>;
   size_t smem = 0;
   const int grid = tma_grid(k, tt, ceil_div(n / 16, tt.tu), &smem);
-  k<<<grid, 256, smem, st>>>(t, n, tt, out, flag);
+  launch_k(k, grid, 256, smem, st, t, n, tt, out, flag);
   return check_cuda(cudaGetLastError(), "dr_tma_kernel launch");
 }
 
