@@ -51,13 +51,16 @@ inline bool balanced_grids() {
 // PdlScope, launch_k sets cudaLaunchAttributeProgrammaticStreamSerialization,
 // so each kernel's launch and CTA ramp overlap the tail of the one before it;
 // every such kernel waits for its predecessor at entry (comm_aborted).
-// ZPP_PDL=0 turns it off (A/B).
+// Opt-in (ZPP_PDL=1): measured no faster on 4 B200s (qgZ bucket 2x2 195.3 vs
+// 192.8 us, 1x4 130.7 vs 132.2, 2x1 258.8 vs 255.4; 40-layer qwZ forward
+// 16.1 ms both; profiles/r2/pdl_ab_r2.jsonl) -- the gaps between the chain's
+// kernels are barrier skew, not launch latency.
 inline thread_local bool t_pdl = false;
 
 inline bool pdl_enabled() {
   static const bool v = [] {
     const char* e = getenv("ZPP_PDL");
-    return !(e && e[0] == '0');
+    return e && e[0] == '1';
   }();
   return v;
 }
