@@ -629,15 +629,7 @@ int zpp_qgz_reduce_scatter_buckets(zpp_comm_t c, size_t sym_offset, const void* 
   // the buckets of a 1-GPU world (no NVLink wait to hide: 7B stream 15.7 vs
   // 11.6 ms).
   // ZPP_QGZ_XB=0 disables it, ZPP_QGZ_XB=2 forces it (A/B).
-  // ZPP_QGZ_XB_LATE=1 (with a second hop): K1 of bucket b+1 starts after
-  // K2 of bucket b instead of after its group barrier, beside the cross
-  // barrier and K3 only (A/B)
-  static const int xb_late_env = [] {
-    const char* e = getenv("ZPP_QGZ_XB_LATE");
-    return e ? atoi(e) : 0;
-  }();
-  const bool late_mode = xb_late_env == 1 && Y > 1 && stages == 1;
-  const bool xb = n_buckets > 1 && (xb_env == 2 || (xb_env == 1 && ((Y == 1 && X > 1) || late_mode)));
+  const bool xb = n_buckets > 1 && (xb_env == 2 || (xb_env == 1 && Y == 1 && X > 1));
   const bool pipelined = stages > 1 || xb;
   if (pipelined && !c->ev_start) {
     if (!c->side) rc = check_cuda(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking), "side stream");
@@ -779,14 +771,13 @@ int zpp_qgz_reduce_scatter_buckets(zpp_comm_t c, size_t sym_offset, const void* 
     rc = barrier(c, 1, kBarrierTimeoutMs, flag, st);
     if (rc) return rc;
     trace_mark(c, TR_BARRIER, st);
-    const bool late = pipelined && late_mode && s + 1 < units;
-    if (pipelined && s + 1 < units && !late) {
+    if (pipelined && s + 1 < units) {
       if ((rc = check_cuda(cudaEventRecord(c->ev_bar, st), "record"))) return rc;
       if ((rc = check_cuda(cudaStreamWaitEvent(c->side, c->ev_bar, 0), "wait"))) return rc;
       if ((rc = k1(s + 1, c->side))) return rc;
       if ((rc = check_cuda(cudaEventRecord(c->ev_k1, c->side), "record"))) return rc;
     }
-    SmBudget budget(pipelined && !share && !late && s + 1 < units ? sm_count() - k1_sms : 0);
+    SmBudget budget(pipelined && !share && s + 1 < units ? sm_count() - k1_sms : 0);
     OccCap cap(share && s + 1 < units ? k2_occ_env : 0);
     // K2: the X messages for this rank, ascending local source -- pushed into
     // this rank's receive region by the group's K1s, or pulled from the peers
@@ -856,14 +847,6 @@ int zpp_qgz_reduce_scatter_buckets(zpp_comm_t c, size_t sym_offset, const void* 
                       /*validate=*/false);
     if (rc) return rc;
     trace_mark(c, TR_K2, st);
-    if (late) {  // K1(s+1) beside the cross barrier and K3(s): its send half was
-                 // last read by peers' K2(s-1), which precedes their barrier(s)
-      if ((rc = check_cuda(cudaEventRecord(c->ev_bar, st), "record"))) return rc;
-      if ((rc = check_cuda(cudaStreamWaitEvent(c->side, c->ev_bar, 0), "wait"))) return rc;
-      if ((rc = k1(s + 1, c->side))) return rc;
-      if ((rc = check_cuda(cudaEventRecord(c->ev_k1, c->side), "record"))) return rc;
-    }
-    SmBudget k3budget(late ? sm_count() - k1_sms : t_sm_cap);
     rc = barrier(c, 2, kBarrierTimeoutMs, flag, st);
     if (rc) return rc;
     trace_mark(c, TR_BARRIER, st);

@@ -46,8 +46,6 @@ def test_two_gpus_bucket_pipeline_forced():
     in share placement: the stream and layer cases of dist_worker stay
     bit-exact on the code paths the defaults skip at this shape."""
     _run(2, 1, 2, env={"ZPP_QGZ_XB": "2", "ZPP_QWZ_PREFETCH_MODE": "share"})
-    # K1 of bucket b+1 beside the cross barrier and K3 of bucket b
-    _run(2, 1, 2, env={"ZPP_QGZ_XB_LATE": "1"})
 
 
 def test_four_gpus_2x2():
