@@ -2112,6 +2112,208 @@ drq_tbl_kernel(SrcTable src, int64_t n, int lg1, int64_t n_blocks_out, uint8_t* 
   if constexpr (HOP) __threadfence_system();  // the stores to peers are performed before the cross barrier's release
 }
 
+// K2 through a certified fp32 estimate (INT4 sources with fp32 absmax,
+// 512-multiple input blocks, INT4/512 output).  The reference's value per
+// element is the f64 fold acc = RN64(...RN64(T0[c0] + T1[c1])...) of the
+// products Tj[c] = RN64(+0.0 + RN64(c * s_j)) (zs/quantizer.py:237,255-257),
+// and only two things about it reach the output: the block's exact
+// absmax M = max |acc| (stored in f64) and each code rint(RN64(acc * inv)),
+// inv = RN64(7/M) (:218-226).  Here every element is first folded in fp32
+// from per-block fp32 tables RN32(Tj[c]) (one LDS.32 per code, half the
+// shared-memory wavefronts of the f64 tables); with S = sum_j 7 s_j,
+//     |acc32 - acc| <= E = NSRC * 2^-22 * S
+// (NSRC fp32 roundings of the tables and the adds, each <= 2^-24 S, plus the
+// reference's own f64 roundings).  Then:
+//   * absmax: the true argmax has |acc32| >= m32 - 2E (m32 = max |acc32|),
+//     so the exact f64 fold of just those candidates (usually one element)
+//     gives M bit-exactly;
+//   * codes: with t = acc32 * RN32(inv) and e = t - rint(t) from one FFMA,
+//     |t - acc*inv| < E*inv + 2^-20 =: G, so |e| <= 0.5 - G proves the code;
+//     any other element (a near tie, ~G of them) is redone with the exact f64
+//     fold and the reference's f64 requantization.
+// Blocks whose scales are outside [2^-100, 2^100] (fp32 range/subnormal
+// effects) take the exact f64 fold for every element.  Same bits as drq_tbl.
+template <int NSRC, typename FO = void>
+__global__ void __launch_bounds__(256, std::is_void<FO>::value ? 3 : 2)  // codes out: <= 85 registers, 3 CTAs/SM
+drq_est_kernel(SrcTable src, int64_t n, int lg1, int64_t n_blocks_out, uint8_t* __restrict__ codes,
+               double* __restrict__ absmax, uint32_t* __restrict__ flag, FO* __restrict__ final_out, int span_ok) {
+  if (comm_aborted(flag)) return;
+  constexpr int QMAX = 7;
+  __shared__ __align__(256) float tbl_all[8][NSRC][64];  // 256-byte slot per (warp, source), 16 entries used
+  __shared__ __align__(64) float fo_all[8][16];
+  const int tl = threadIdx.x & 31;
+  const int wid = threadIdx.x >> 5;
+  const uint32_t slot0 = (uint32_t)__cvta_generic_to_shared(&tbl_all[wid][0][0]);
+  float* fo_tbl = fo_all[wid];
+  const int64_t nwarp = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const bool span = span_ok && NSRC > 1 && std::is_same<FO, float>::value && (n & 511) == 0;
+  bool bad = false;
+  uint2 w[NSRC], wn[NSRC];
+  float m[NSRC], mn[NSRC];
+  auto load = [&](int64_t b, uint2 (&wv)[NSRC], float (&mv)[NSRC]) {
+    const int64_t e0 = b * 512 + (int64_t)tl * 16;
+    const bool blk = b < n_blocks_out, ok = blk && e0 < n;
+#pragma unroll
+    for (int j = 0; j < NSRC; ++j) {
+      wv[j] = !ok ? make_uint2(0, 0)
+              : span ? int4_span_pieces_g(src.codes[j] + b * 256, tl)
+                     : __ldg(reinterpret_cast<const uint2*>(src.codes[j]) + (e0 >> 4));
+      mv[j] = blk ? __ldg(reinterpret_cast<const float*>(src.absmax[j]) + ((b * 512) >> lg1)) : 0.0f;
+    }
+  };
+  int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  load(b, wn, mn);
+  for (; b < n_blocks_out; b += nwarp) {
+    const int64_t e0 = b * 512 + (int64_t)tl * 16;
+    const bool active = e0 < n;
+#pragma unroll
+    for (int j = 0; j < NSRC; ++j) {
+      w[j] = wn[j];
+      m[j] = mn[j];
+    }
+    load(b + nwarp, wn, mn);
+#pragma unroll
+    for (int j = 0; j < NSRC; ++j) bad |= has_nibble_8(w[j].x) | has_nibble_8(w[j].y);
+    // exact f64 scales (warp-uniform) and the error budget
+    double sc[NSRC];
+    double S = 0.0;
+    bool wild = false;
+#pragma unroll
+    for (int j = 0; j < NSRC; ++j) {
+      sc[j] = div_q_f32<QMAX>(m[j]);
+      S += 7.0 * sc[j];
+      wild |= sc[j] != 0.0 && !(sc[j] >= 0x1p-100 && sc[j] <= 0x1p100);
+    }
+    const double E = S * (double)NSRC * 0x1p-22 * (1.0 + 0x1p-20);
+    // fp32 tables: lanes 16h + k build entry k of source 2p + h
+    __syncwarp();  // the previous block's lookups are done
+#pragma unroll
+    for (int p = 0; p < (NSRC + 1) / 2; ++p) {
+      const int j = 2 * p + (tl >> 4);
+      if (j < NSRC) {
+        const double sj = (tl >> 4) ? sc[2 * p + 1 < NSRC ? 2 * p + 1 : 2 * p] : sc[2 * p];
+        tbl_all[wid][j][tl & 15] = __double2float_rn(__dadd_rn(0.0, __dmul_rn((double)((tl & 15) - 8), sj)));
+      }
+    }
+    __syncwarp();
+    // exact f64 fold of element i of this lane (the reference's arithmetic)
+    auto exact = [&](int i) -> double {
+      const int sh = 4 * (i & 7);
+      double a = 0.0;
+#pragma unroll
+      for (int j = 0; j < NSRC; ++j) {
+        const uint32_t word = (i < 8) ? w[j].x : w[j].y;
+        const int c = (int)(((word >> sh) & 0xFu) ^ 8u) - 8;
+        const double pr = __dmul_rn((double)c, sc[j]);
+        a = j == 0 ? __dadd_rn(0.0, pr) : __dadd_rn(a, pr);
+      }
+      return a;
+    };
+    // fp32 fold through the tables (element order as fold16_tbl4)
+    float acc[16];
+#pragma unroll
+    for (int j = 0; j < NSRC; ++j) {
+      const uint32_t slot = slot0 + j * 256;
+      const uint32_t ww[2] = {w[j].x, w[j].y};
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const uint32_t bb = ww[k] ^ 0x88888888u;
+        const uint32_t ev = (bb << 2) & 0x3C3C3C3Cu;  // 4 * (low nibble) per byte
+        const uint32_t od = (bb >> 2) & 0x3C3C3C3Cu;  // 4 * (high nibble) per byte
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          float v0, v1;
+          asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v0) : "r"(__byte_perm(ev, slot, 0x7650 + q)) : "memory");
+          asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v1) : "r"(__byte_perm(od, slot, 0x7650 + q)) : "memory");
+          if (j == 0) {
+            acc[8 * k + 2 * q] = v0;
+            acc[8 * k + 2 * q + 1] = v1;
+          } else {  // one FADD2 for the pair
+            const float2 r = fadd2(make_float2(acc[8 * k + 2 * q], acc[8 * k + 2 * q + 1]), make_float2(v0, v1));
+            acc[8 * k + 2 * q] = r.x;
+            acc[8 * k + 2 * q + 1] = r.y;
+          }
+        }
+      }
+    }
+    // exact absmax: candidates within 2E of the estimated max
+    float lm = 0.0f;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) lm = fmaxf(lm, fabsf(acc[i]));
+    const float m32 = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(lm)));
+    const double thr = wild ? -1.0 : (double)m32 - 2.0 * E;
+    double lmax = 0.0;
+    if ((double)lm >= thr) {  // rare: the lanes holding a candidate (every lane of a wild block)
+#pragma unroll
+      for (int i = 0; i < 16; ++i)  // unrolled: acc[] stays in registers
+        if (wild || (double)fabsf(acc[i]) >= thr) lmax = dmax_nn(lmax, fabs(exact(i)));
+    }
+    const double mx = warp_max_nonneg(lmax);
+    if (tl == 0) {
+      absmax[b] = mx;
+      if (!(mx <= DBL_MAX)) raise_flag(flag, FLAG_NONFINITE);
+    }
+    const double inv = mx > 0.0 ? __ddiv_rn((double)QMAX, mx) : 0.0;
+    const float inv32 = __double2float_rn(inv);
+    // |e| <= 0.5 - G proves the code; G >= 0.5 (heavy cancellation) sends every element to the exact path
+    const float guard = wild ? -1.0f : __double2float_rd(0.5 - (E * inv + 0x1p-20));
+    uint32_t q[16];
+    float emax = 0.0f;
+    {
+      const float2 inv2 = make_float2(inv32, inv32), m2 = make_float2(kMagic23, kMagic23);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {  // FFMA2 / FADD2 / FFMA2 per pair
+        const float2 x = make_float2(acc[2 * i], acc[2 * i + 1]);
+        const float2 u = ffma2(x, inv2, m2);
+        const float2 nk = fadd2(m2, make_float2(-u.x, -u.y));
+        const float2 ee = ffma2(x, inv2, nk);
+        q[2 * i] = __float_as_uint(u.x);
+        q[2 * i + 1] = __float_as_uint(u.y);
+        emax = fmaxf(emax, fmaxf(fabsf(ee.x), fabsf(ee.y)));
+      }
+    }
+    if (!(emax <= guard)) {  // rare: the reference's requantization for the unproven elements
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {  // unrolled: q[] stays in registers
+        const float ei = __fmaf_rn(acc[i], inv32, kMagic23 - __uint_as_float(q[i]));
+        if (!(fabsf(ei) <= guard)) q[i] = (uint32_t)__double2loint(__dadd_rn(__dmul_rn(exact(i), inv), kMagic52));
+      }
+    }
+    if constexpr (std::is_void<FO>::value) {
+      // inactive lanes hold zero codes: the zero padding of a partial last block
+      uint32_t q0[8], q1[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        q0[i] = q[i];
+        q1[i] = q[8 + i];
+      }
+      *reinterpret_cast<uint2*>(codes + (e0 >> 4) * 8) = make_uint2(pack8_int4(q0), pack8_int4(q1));
+    } else {
+      static_assert(sizeof(FO) == 4, "fp32 final output");
+      const double s2 = scale_of<4>(mx);
+      __syncwarp();  // the previous block's FO lookups are done
+      if (tl < 16) fo_tbl[tl] = __double2float_rn(__dadd_rn(0.0, __dmul_rn((double)(tl - 8), s2)));
+      __syncwarp();
+      if (active) {
+        float v[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = fo_tbl[((int)(q[i] << 28) >> 28) + 8];  // low nibble = code
+        if (span) {
+          float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(final_out) + b * 512);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) dst[k * 32 + tl] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+        } else {
+          float* dst = reinterpret_cast<float*>(final_out) + e0;
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            reinterpret_cast<float4*>(dst)[k] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+        }
+      }
+    }
+  }
+  if (bad) raise_flag(flag, FLAG_BADCODE);
+}
+
 // K3 fixed fan-in fast path (the qgZ hop-2 fold, zs/collectives.py:536-544):
 // NSRC sources known at compile time, power-of-two block, fp32/f64 output;
 // lane = 16 contiguous elements, grid-stride, next unit's codes and absmax

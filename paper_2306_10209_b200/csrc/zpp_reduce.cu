@@ -121,6 +121,16 @@ static bool drq_fast_ok(int n_src, int64_t n, int64_t in_block, int64_t out_bloc
          (in_block & (in_block - 1)) == 0 && (n_src == 1 || n_src == 2 || n_src == 4 || n_src == 8);
 }
 
+// ZPP_K2=tbl (development A/B only): K2 through the f64 product tables
+// instead of the certified fp32 estimate
+static bool k2_est_on() {
+  static const bool v = [] {
+    const char* e = getenv("ZPP_K2");
+    return !(e && e[0] == 't');
+  }();
+  return v;
+}
+
 // ZPP_NO_TBL=1 (development A/B only): INT4 folds without product tables
 bool tbl_off() {
   static const bool off = [] {
@@ -145,8 +155,20 @@ static int run_drq_fast(const SrcTable& t, int n_src, int64_t n, int64_t in_bloc
   const int lg1 = __builtin_ctzll((unsigned long long)in_block);
   // INT4 sources with one scale per 512-element warp tile: product tables
   const bool tbl = IBITS == 4 && in_block % 512 == 0 && !tbl_off();
+  // INT4 -> INT4/512 through the certified fp32 estimate (drq_est_kernel);
+  // ZPP_K2=tbl keeps the f64 product tables (A/B)
+  constexpr bool can_est = IBITS == 4 && OBITS == 4 && (std::is_void<FO>::value || std::is_same<FO, float>::value);
+  const bool est = can_est && tbl && k2_est_on();
 #define ZPP_FAST(NS)                                                                            \
   {                                                                                             \
+    if constexpr (can_est) {                                                                    \
+      if (est) {                                                                                \
+        auto k = drq_est_kernel<NS, FO>;                                                        \
+        const int grid = grid_for(k, 256, ceil_div(nbo, 8));                                    \
+        launch_k(k, grid, 256, 0, st, t, n, lg1, nbo, codes, absmax, flag, final_out, span_on() ? 1 : 0); \
+        return check_cuda(cudaGetLastError(), "drq_est_kernel launch");                         \
+      }                                                                                         \
+    }                                                                                           \
     if (tbl) {                                                                                  \
       auto k = tbl_split() == 2 && NS == 4 ? drq_tbl_kernel<OBITS, NS, FO, (NS == 4 ? 2 : NS)>   \
                                              : drq_tbl_kernel<OBITS, NS, FO>;                   \

@@ -400,6 +400,51 @@ def test_fused_fixed_fanin_fast_path(n_src):
         zpp.fused_dequant_reduce_quant(qs, zpp.QuantConfig(bit_width=4, block_size=512))
 
 
+@pytest.mark.parametrize("n_src", [1, 2, 4, 8])
+@pytest.mark.parametrize("case", ["cancel", "near_cancel", "spread", "tiny", "huge", "ties", "zeros"])
+def test_fused_int4_estimate_adversarial(n_src, case):
+    """K2 INT4 -> INT4/512 goes through a certified fp32 estimate
+    (drq_est_kernel) with exact f64 redo of absmax candidates and near ties:
+    the cases that stress the certificate -- exact and near cancellation
+    between sources (every element a redo), scales 2^40 apart, scales below
+    2^-100 and above 2^100 (the exact path for the whole block), exact ties
+    in the requantization, all-zero blocks -- still give the reference's codes
+    and f64 scales bit for bit (zs/quantizer.py:241-258)."""
+    zpp = _zpp()
+    rng = np.random.default_rng(n_src * 100 + ["cancel", "near_cancel", "spread", "tiny", "huge", "ties",
+                                                "zeros"].index(case))
+    n = 8 * 512 + 256
+    cfg = zpp.QuantConfig(bit_width=4, block_size=512)
+    base = rng.normal(size=n)
+    vals = []
+    for k in range(n_src):
+        if case == "cancel":
+            v = base * (1 if k % 2 == 0 else -1)
+        elif case == "near_cancel":
+            v = base * (1 if k % 2 == 0 else -1) + rng.normal(size=n) * 1e-3
+        elif case == "spread":
+            v = rng.normal(size=n) * 2.0 ** (40 * (k % 2) - 20)
+        elif case == "tiny":
+            v = rng.normal(size=n) * 1e-33
+        elif case == "huge":
+            v = rng.normal(size=n) * 1e33
+        elif case == "ties":
+            v = rng.integers(-7, 8, size=n).astype(np.float64) * 0.5  # lattice values: exact ties after the fold
+        else:
+            v = np.zeros(n)
+            v[:512] = rng.normal(size=512) if k == 0 else 0.0
+        vals.append(v.astype(np.float32).astype(np.float64))
+    qs = [zpp.quantize(torch.from_numpy(v).float().cuda(), cfg) for v in vals]
+    f = zpp.fused_dequant_reduce_quant(qs, cfg)
+    ins = []
+    for v in vals:
+        c, sc, _ = O.quantize(v, 4, 512)
+        ins.append((c, sc, n, 4, 512))
+    c, sc, _ = O.fused_dequant_reduce_quant(ins, 4, 512)
+    assert np.array_equal(f.codes.cpu().numpy(), c), case
+    assert np.array_equal(f.scales.cpu().numpy().view(np.uint64), np.asarray(sc).view(np.uint64)), case
+
+
 @pytest.mark.parametrize("bits,block", [(8, 64), (4, 32), (8, 2048)])
 def test_to_bytes_device_pack_matches_reference_layout(bits, block):
     """zpp_wire_pack (to_bytes on the device) == the reference's layout built
