@@ -121,12 +121,16 @@ static bool drq_fast_ok(int n_src, int64_t n, int64_t in_block, int64_t out_bloc
          (in_block & (in_block - 1)) == 0 && (n_src == 1 || n_src == 2 || n_src == 4 || n_src == 8);
 }
 
-// ZPP_K2=tbl (development A/B only): K2 through the f64 product tables
-// instead of the certified fp32 estimate
+// ZPP_K2=est (opt-in): K2 through the certified fp32 estimate
+// (drq_est_kernel) instead of the f64 product tables.  Bit-exact (tests), but
+// measured slower: X = 4 62.6 vs 51.2 us, X = 2 87.2 vs 56.2 us, qgZ 2x2
+// bucket 224.7 vs 194.5 us (profiles/r2/k2_est_ab_r2.jsonl): the block's
+// argmax is always an absmax candidate, so every warp runs a divergent exact
+// f64 fold per block, which costs more than the fp32 fold saves.
 static bool k2_est_on() {
   static const bool v = [] {
     const char* e = getenv("ZPP_K2");
-    return !(e && e[0] == 't');
+    return e && e[0] == 'e';
   }();
   return v;
 }
@@ -155,8 +159,8 @@ static int run_drq_fast(const SrcTable& t, int n_src, int64_t n, int64_t in_bloc
   const int lg1 = __builtin_ctzll((unsigned long long)in_block);
   // INT4 sources with one scale per 512-element warp tile: product tables
   const bool tbl = IBITS == 4 && in_block % 512 == 0 && !tbl_off();
-  // INT4 -> INT4/512 through the certified fp32 estimate (drq_est_kernel);
-  // ZPP_K2=tbl keeps the f64 product tables (A/B)
+  // INT4 -> INT4/512 through the certified fp32 estimate (drq_est_kernel)
+  // only with ZPP_K2=est (measured slower than the f64 product tables)
   constexpr bool can_est = IBITS == 4 && OBITS == 4 && (std::is_void<FO>::value || std::is_same<FO, float>::value);
   const bool est = can_est && tbl && k2_est_on();
 #define ZPP_FAST(NS)                                                                            \

@@ -445,6 +445,20 @@ def test_fused_int4_estimate_adversarial(n_src, case):
     assert np.array_equal(f.scales.cpu().numpy().view(np.uint64), np.asarray(sc).view(np.uint64)), case
 
 
+def test_fused_int4_estimate_kernel_opt_in():
+    """The same adversarial cases, the fixed fan-in cases and the golden K2
+    cases through the opt-in certified-estimate K2 (ZPP_K2=est)."""
+    import os
+    import subprocess
+    import sys
+
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider", os.path.abspath(__file__),
+                        "-k", "int4_estimate_adversarial or fused_fixed_fanin or fused_golden"],
+                       env={**os.environ, "ZPP_K2": "est"}, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout
+
+
 @pytest.mark.parametrize("bits,block", [(8, 64), (4, 32), (8, 2048)])
 def test_to_bytes_device_pack_matches_reference_layout(bits, block):
     """zpp_wire_pack (to_bytes on the device) == the reference's layout built
