@@ -206,8 +206,9 @@ int zpp_qgz_reduce_scatter(zpp_comm_t comm, size_t sym_offset, const void* grad,
  * stream cut into buckets, BASELINE configs[3]; zs/engine.py:455-506 reduces
  * a model's gradients this way): bucket b is one zpp_qgz_reduce_scatter of
  * grad[b*n, (b+1)*n) into out[b*n/W, (b+1)*n/W).  Same results as n_buckets
- * separate calls; K1 (quantize, hop-1 push) of bucket b+1 runs on the
- * communicator's side stream beside K2/K3 of bucket b.  No reference
+ * separate calls.  With one group (Y = 1) K1 of bucket b+1 runs on the
+ * communicator's side stream beside the pulling K2 of bucket b; with a
+ * second hop the buckets run back to back (measured faster).  No reference
  * counterpart beyond the per-bucket qgz_2hop (zs/collectives.py:464-569). */
 int zpp_qgz_reduce_scatter_buckets(zpp_comm_t comm, size_t sym_offset, const void* grad, int dtype, int64_t n,
                                    int n_buckets, int stages, int reorder, int intra_bits, int64_t intra_block,

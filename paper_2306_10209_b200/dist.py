@@ -343,8 +343,10 @@ class Communicator:
         tail bucket is zero-padded as zs/engine.py:465-466 pads the whole
         tensor (one device copy into a staging buffer kept by the
         communicator).  The full buckets are one zpp_qgz_reduce_scatter_buckets
-        call: K1 of bucket b+1 runs on the communicator's side stream beside
-        K2/K3 of bucket b (same results as separate calls)."""
+        call (same results as separate calls); with one group (hop 2 a
+        self-send) K1 of bucket b+1 runs on the communicator's side stream
+        beside the pulling K2 of bucket b, otherwise buckets run back to back
+        (the measured better choice for each layout)."""
         self._usable()
         n_total = int(grads.numel())
         full, tail, tail_pad, n_out = self.stream_layout(n_total)
