@@ -815,13 +815,35 @@ int zpp_qgz_reduce_scatter_buckets(zpp_comm_t c, size_t sym_offset, const void* 
       }
     }
     bool handled = false;
+    // One GPU per group with one codec for both hops: hop 2 sends K1's codes
+    // as they are (hop_absmax_x1_kernel has the proof) and only the f64
+    // absmax is computed; ZPP_QGZ_X1=0 runs the full K2 (A/B)
+    static const int x1_env = [] {
+      const char* e = getenv("ZPP_QGZ_X1");
+      return e ? atoi(e) : 1;
+    }();
+    // Not when pipelined: K3 of the cross peers then reads this rank's send
+    // region, whose half K1(s+1) would rewrite right after the (single-member,
+    // skipped) group barrier(s), before the peers' K3(s-1) is known done.
+    const bool x1 = x1_env != 0 && !pipelined && X == 1 && intra_bits == inter_bits &&
+                    intra_block == inter_block && in_abs == ZPP_F32;
+    if (x1) {
+      const int64_t nb = msg_elems / inter_block;
+      const float* m32 = reinterpret_cast<const float*>(c->local + base + l.send_abs);
+      double* m64 = reinterpret_cast<double*>(c->local + base + l.hop_abs);
+      const int grid = (int)std::min<int64_t>(4 * sm_count(), std::max<int64_t>(1, ceil_div(nb, 256)));
+      if (inter_bits == 4) launch_k(hop_absmax_x1_kernel<7>, grid, 256, 0, st, m32, nb, m64, flag);
+      else launch_k(hop_absmax_x1_kernel<127>, grid, 256, 0, st, m32, nb, m64, flag);
+      if ((rc = check_cuda(cudaGetLastError(), "hop_absmax_x1_kernel launch"))) return rc;
+      handled = true;
+    }
     // Hop 2 by push (with a pushed hop 1): K2 stores segment c of its output
     // straight into rank (c, loc)'s hop-2 receive slot for this node, over
     // NVLink, and K3 folds local HBM.  The slot was last read by that rank's
     // K3 of the unit before the previous one, which precedes its cross
     // barrier of the previous unit, which this K2 follows.
     bool hop2_pushed = false;
-    if (push && hop2_push) {
+    if (!x1 && push && hop2_push) {
       HopDst hd{};
       const size_t seg_code_bytes = (size_t)code_bytes(L, inter_bits, inter_block);
       for (int g = 0; g < Y; ++g) {
@@ -855,7 +877,8 @@ int zpp_qgz_reduce_scatter_buckets(zpp_comm_t c, size_t sym_offset, const void* 
     for (int g = 0; g < Y; ++g) {
       const uint8_t* p = hop2_pushed ? c->local + base : c->peers[g * X + loc] + base;
       const int slot = hop2_pushed ? g : node;
-      codes[g] = p + l.hop_codes + (size_t)code_bytes(L, inter_bits, inter_block) * slot;
+      // X = 1: the segment's codes are K1's, in the send region ([0][c][e])
+      codes[g] = p + (x1 ? l.send_codes : l.hop_codes) + (size_t)code_bytes(L, inter_bits, inter_block) * slot;
       absmax[g] = p + l.hop_abs + (size_t)(L / inter_block) * 8 * slot;
     }
     handled = false;

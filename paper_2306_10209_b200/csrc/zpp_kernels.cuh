@@ -2314,6 +2314,21 @@ drq_est_kernel(SrcTable src, int64_t n, int lg1, int64_t n_blocks_out, uint8_t* 
   if (bad) raise_flag(flag, FLAG_BADCODE);
 }
 
+// qgZ with one GPU per group (X = 1): hop 1 is a self-send, and K2 would
+// requantize the dequantized codes of a single source with the same block
+// (zs/quantizer.py:241-258).  That reproduces every code exactly -- the max
+// element's code is +-QMAX, so maxabs = RN64(QMAX*s) and
+// RN64(RN64(c*s) * RN64(QMAX/maxabs)) = c*(1 + e) with |c*e| <= QMAX*2^-50 --
+// so hop 2 sends K1's codes as they are, and this kernel writes only the f64
+// block absmax RN64(QMAX * RN64(m/QMAX)) that K2 would have produced.
+template <int QMAX>
+__global__ void __launch_bounds__(256)
+hop_absmax_x1_kernel(const float* __restrict__ m, int64_t nb, double* __restrict__ out, uint32_t* __restrict__ flag) {
+  if (comm_aborted(flag)) return;
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x)
+    out[b] = __dmul_rn((double)QMAX, div_q_f32<QMAX>(__ldg(m + b)));
+}
+
 // K3 fixed fan-in fast path (the qgZ hop-2 fold, zs/collectives.py:536-544):
 // NSRC sources known at compile time, power-of-two block, fp32/f64 output;
 // lane = 16 contiguous elements, grid-stride, next unit's codes and absmax
