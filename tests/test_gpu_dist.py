@@ -21,10 +21,14 @@ def _free_port():
 
 
 def _run(nproc, group, stages, env=None, worker="dist_worker.py", extra=()):
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
-           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
-           os.path.join(HERE, worker), "--group", str(group), *(["--stages", str(stages)] if stages else []), *extra]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env={**os.environ, **(env or {})})
+    for attempt in range(3):  # the free port can be taken between probing and binding
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+               "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+               os.path.join(HERE, worker), "--group", str(group), *(["--stages", str(stages)] if stages else []),
+               *extra]
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env={**os.environ, **(env or {})})
+        if r.returncode == 0 or "EADDRINUSE" not in r.stderr:
+            break
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
     return r.stdout
 
