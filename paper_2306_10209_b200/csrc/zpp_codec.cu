@@ -213,7 +213,7 @@ static int dispatch_qpush(const T* x, const SwizzleAddr& addr, int n_msg, int fi
 
 int launch_quantize_push(const void* x, int dtype, const AddrSpec& a, int64_t n_out, int bits, int64_t block,
                          uint8_t* const* dst_codes, uint8_t* const* dst_absmax, int64_t msg_blocks, int first,
-                         uint32_t* flag, cudaStream_t st, bool* handled) {
+                         int self_msg, uint32_t* flag, cudaStream_t st, bool* handled) {
   *handled = false;
   if (n_out == 0 || !a.swizzle || !aligned16(x) || a.X > kMaxPush) return ZPP_OK;
   if (a.L / block >= (1ll << 31) || (int64_t)a.X * a.Y * (a.L / block) >= (1ll << 31)) return ZPP_OK;
@@ -227,6 +227,12 @@ int launch_quantize_push(const void* x, int dtype, const AddrSpec& a, int64_t n_
     d.absmax[j] = j < a.X ? dst_absmax[j] : nullptr;
   }
   d.mb = FastDiv::make((uint32_t)msg_blocks);
+  // ZPP_PUSH_STAGE_SELF=1 (A/B): stage and bulk-store the kept message too
+  static const bool stage_self = [] {
+    const char* e = getenv("ZPP_PUSH_STAGE_SELF");
+    return e && e[0] == '1';
+  }();
+  d.self_msg = stage_self ? -1 : self_msg;
   if (ceil_div(n_out, block) != (int64_t)a.X * msg_blocks) return fail(ZPP_ERR_VALIDATION, "push: bad message size");
   const auto* xx = x;
 #define ZPP_P(T)                                                                                                 \

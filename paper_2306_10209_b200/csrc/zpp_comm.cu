@@ -743,7 +743,7 @@ int zpp_qgz_reduce_scatter_buckets(zpp_comm_t c, size_t sym_offset, const void* 
       // rank loc starts with the message for local peer loc+1: the group's
       // ranks begin on different destinations
       const int rc1 = launch_quantize_push(g, dtype, a, (int64_t)W * L, intra_bits, intra_block, dc, da, msg_blocks,
-                                           (loc + 1) % X, flag, on, &handled);
+                                           (loc + 1) % X, loc, flag, on, &handled);
       if (rc1 || handled) return rc1;
       return fail(ZPP_ERR_VALIDATION, "qgZ: no push path for this shape");
     }

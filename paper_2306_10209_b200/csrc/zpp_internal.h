@@ -31,7 +31,7 @@ int launch_quantize(const void* x, int dtype, const AddrSpec& a, int64_t n_out, 
 // the messages starting at `first`.  *handled = false when
 // the shape has no push path (the caller then quantizes locally).
 int launch_quantize_push(const void* x, int dtype, const AddrSpec& a, int64_t n_out, int bits, int64_t block,
-                         uint8_t* const* dst_codes, uint8_t* const* dst_absmax, int64_t msg_blocks, int first,
+                         uint8_t* const* dst_codes, uint8_t* const* dst_absmax, int64_t msg_blocks, int first, int self_msg,
                          uint32_t* flag, cudaStream_t st, bool* handled);
 int launch_quantize_deq(const void* x, int dtype, int64_t n, int bits, int64_t block, uint8_t* codes, void* absmax,
                         void* out, uint32_t* flag, cudaStream_t st, bool* handled);

@@ -1857,6 +1857,7 @@ struct PushDst {
   uint8_t* codes[kMaxPush];  // peer j's receive slot for this rank's message (codes)
   uint8_t* absmax[kMaxPush]; // ... and its fp32 absmax
   FastDiv mb;                // send blocks per message
+  int self_msg;              // the message this rank keeps (its own slot): stored directly, not staged
 };
 
 template <typename T, int BITS, int LANES, int EPL>
@@ -1883,17 +1884,32 @@ quantize_push_kernel(const T* __restrict__ x, SwizzleAddr addr, int n_msg, int f
   const int64_t tiles = tpm * n_msg;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  int it = 0;
-  for (int64_t v = gw; v < tiles; v += nw, ++it) {
+  int it = 0;  // staged tiles so far
+  for (int64_t v = gw; v < tiles; v += nw) {
+    int j = (int)(v % n_msg) + first;
+    if (j >= n_msg) j -= n_msg;
+    const int64_t off0 = (v / n_msg) * WT;  // first block of the tile inside message j
+    const int nb = (int)min((int64_t)WT, mbs - off0);
+    if (j == dst.self_msg) {
+      // the message this rank keeps: quantize straight into its slot in local
+      // HBM, like K1 without the push (no staging, no bulk store)
+      uint8_t* const cb = dst.codes[j] + off0 * BB;
+      float* const ab = reinterpret_cast<float*>(dst.absmax[j]) + off0;
+#pragma unroll 1
+      for (int r = 0; r < R; ++r) {
+        const int bl = r * TPW + team;
+        TeamIn<T, EPL> in;
+        quant_load<T, LANES, EPL, SwizzleAddr>(x, addr, (int64_t)j * mbs + off0 + bl, bl < nb, tl, in);
+        quant_compute<T, BITS, LANES, EPL, false>(x, in, bl, bl < nb, tl, cb, ab, flag, nullptr);
+      }
+      continue;
+    }
     const int buf = it & 1;
     if (it >= 2) {
       if (lane == 0) bulk_wait_read<1>();  // the stores issued from this buffer two tiles ago have read it
       __syncwarp();
     }
-    int j = (int)(v % n_msg) + first;
-    if (j >= n_msg) j -= n_msg;
-    const int64_t off0 = (v / n_msg) * WT;  // first block of the tile inside message j
-    const int nb = (int)min((int64_t)WT, mbs - off0);
+    ++it;
 #pragma unroll 1
     for (int r = 0; r < R; ++r) {
       const int bl = r * TPW + team;
