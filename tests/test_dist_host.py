@@ -62,3 +62,23 @@ def test_layout_regions_are_disjoint_and_aligned():
 
 def test_exchange_handles_without_process_group():
     assert exchange_handles(b"x" * 64) == b"x" * 64
+
+
+def test_stream_layout_pads_the_tail_like_the_reference():
+    """Communicator.stream_layout (host arithmetic only): a 7B gradient stream
+    in 256 MiB buckets is 52 full buckets plus a 20,678,144-element tail,
+    zero-padded to a multiple of W * S * max(block) (zs/engine.py:465-466:
+    20,680,704 at W = 8, S = 1, INT4/512); the output holds every
+    bucket's partition followed by the padded tail's."""
+    from types import SimpleNamespace
+
+    from paper_2306_10209_b200.dist import Communicator
+    from paper_2306_10209_b200.quantizer import QuantConfig
+
+    cfg = QuantConfig(bit_width=4, block_size=512)
+    for world, stages, want_pad in ((8, 1, 20_680_704), (4, 1, 20_678_656), (2, 2, 20_678_656), (1, 1, 20_678_144)):
+        fake = SimpleNamespace(qgz_elems=134_217_728, world=world, qgz_stages=stages, qgz_cfg=cfg, qgz_intra_cfg=cfg)
+        full, tail, tail_pad, n_out = Communicator.stream_layout(fake, 7_000_000_000)
+        assert (full, tail) == (52, 20_678_144)
+        assert tail_pad == want_pad and tail_pad % (world * stages * 512) == 0 and tail_pad >= tail
+        assert n_out == (52 * 134_217_728 + tail_pad) // world
